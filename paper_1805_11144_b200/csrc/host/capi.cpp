@@ -1,0 +1,127 @@
+// capi.cpp — the extern "C" surface of include/neng_gpu.h.  Every entry point
+// catches C++ exceptions and maps them 1:1 onto status codes (the reference's
+// StructuralError/BuildError/RunError, ir.hpp:15-25) with the message kept in
+// a thread-local (neng_last_error) and on the engine (neng_gpu_last_error).
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "engine.hpp"
+#include "neng_gpu.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+neng_status guarded(nengb::Engine* e, F&& f) {
+    auto fail = [&](neng_status s, const char* msg) {
+        g_last_error = msg;
+        if (e) e->last_error = msg;
+        return s;
+    };
+    try {
+        f();
+        return NENG_OK;
+    } catch (const nengb::StructuralError& x) {
+        return fail(NENG_STRUCTURAL_ERROR, x.what());
+    } catch (const nengb::BuildError& x) {
+        return fail(NENG_BUILD_ERROR, x.what());
+    } catch (const nengb::RunError& x) {
+        return fail(NENG_RUN_ERROR, x.what());
+    } catch (const nengb::CudaError& x) {
+        return fail(NENG_CUDA_ERROR, x.what());
+    } catch (const nengb::InvalidArgument& x) {
+        return fail(NENG_INVALID_ARGUMENT, x.what());
+    } catch (const std::bad_alloc&) {
+        return fail(NENG_OUT_OF_MEMORY, "out of memory");
+    } catch (const std::exception& x) {
+        return fail(NENG_INVALID_ARGUMENT, x.what());
+    }
+}
+
+}  // namespace
+
+struct neng_engine {
+    nengb::Engine impl;
+    template <class... A>
+    explicit neng_engine(A&&... a) : impl(std::forward<A>(a)...) {}
+};
+
+extern "C" {
+
+neng_status neng_gpu_create(const neng_planned_model* planned, int32_t batch, int32_t unroll,
+                            const neng_device_cfg* cfg, neng_engine** out) {
+    return guarded(nullptr, [&] {
+        if (!planned || !out) throw nengb::InvalidArgument("neng_gpu_create: null argument");
+        *out = nullptr;
+        nengb::PlannedModel pm = nengb::planned_from_view(*planned);
+        *out = new neng_engine(std::move(pm), batch, unroll, cfg);
+    });
+}
+
+void neng_gpu_destroy(neng_engine* e) { delete e; }
+
+neng_status neng_gpu_run(neng_engine* e, int32_t n_steps, int32_t n_feeds, const neng_feed* feeds,
+                         double* probes_out) {
+    if (!e) return NENG_INVALID_ARGUMENT;
+    return guarded(&e->impl, [&] { e->impl.run(n_steps, n_feeds, feeds, probes_out); });
+}
+
+neng_status neng_gpu_run_device(neng_engine* e, int32_t n_steps, const float* const* d_feeds,
+                                float* const* d_probes, void* stream) {
+    if (!e) return NENG_INVALID_ARGUMENT;
+    return guarded(&e->impl, [&] {
+        e->impl.run_device(n_steps, d_feeds, d_probes, static_cast<cudaStream_t>(stream));
+    });
+}
+
+neng_status neng_gpu_synchronize(neng_engine* e) {
+    if (!e) return NENG_INVALID_ARGUMENT;
+    return guarded(&e->impl, [&] { e->impl.synchronize(); });
+}
+
+neng_status neng_gpu_reset(neng_engine* e) {
+    if (!e) return NENG_INVALID_ARGUMENT;
+    return guarded(&e->impl, [&] { e->impl.reset(); });
+}
+
+neng_status neng_gpu_read_signal(const neng_engine* e, int32_t signal, int32_t batch_index, double* out,
+                                 int64_t capacity, int64_t* n_out) {
+    if (!e) return NENG_INVALID_ARGUMENT;
+    auto* ee = const_cast<neng_engine*>(e);
+    return guarded(&ee->impl, [&] {
+        std::vector<double> v = e->impl.read_signal(signal, batch_index);
+        if (n_out) *n_out = static_cast<int64_t>(v.size());
+        if (out) {
+            if (capacity < static_cast<int64_t>(v.size()))
+                throw nengb::InvalidArgument("read_signal: output capacity too small");
+            std::memcpy(out, v.data(), v.size() * sizeof(double));
+        }
+    });
+}
+
+neng_status neng_gpu_buffer_storage(const neng_engine* e, int32_t buffer, int32_t* mode_out) {
+    if (!e || !mode_out) return NENG_INVALID_ARGUMENT;
+    auto* ee = const_cast<neng_engine*>(e);
+    return guarded(&ee->impl, [&] { *mode_out = e->impl.buffer_storage(buffer); });
+}
+
+int32_t neng_gpu_batch(const neng_engine* e) { return e ? e->impl.batch() : 0; }
+int32_t neng_gpu_unroll(const neng_engine* e) { return e ? e->impl.unroll() : 0; }
+int32_t neng_gpu_steps_completed(const neng_engine* e) { return e ? e->impl.steps_completed() : 0; }
+int32_t neng_gpu_num_probes(const neng_engine* e) { return e ? e->impl.num_probes() : 0; }
+int32_t neng_gpu_mode(const neng_engine* e) { return e ? e->impl.mode() : 0; }
+int64_t neng_gpu_last_launch_count(const neng_engine* e) { return e ? e->impl.last_launches() : 0; }
+
+neng_status neng_gpu_probe_info(const neng_engine* e, int32_t i, int32_t* key, int32_t* dim) {
+    if (!e || i < 0 || i >= e->impl.num_probes()) return NENG_INVALID_ARGUMENT;
+    if (key) *key = e->impl.planned().model.probes[i].key;
+    if (dim) *dim = e->impl.probe_dim(i);
+    return NENG_OK;
+}
+
+const char* neng_gpu_last_error(const neng_engine* e) { return e ? e->impl.last_error.c_str() : ""; }
+const char* neng_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

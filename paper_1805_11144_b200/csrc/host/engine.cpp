@@ -1,0 +1,702 @@
+// engine.cpp — compile a PlannedModel into device storage + a device program,
+// and step it (the B200 counterpart of EngineCore<T>::compile/run/reset/
+// read_signal, proj/src/exec.cpp:41-377).
+#include "engine.hpp"
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <thread>
+#include <unordered_map>
+
+#include "fused.hpp"
+
+namespace nengb {
+
+// kernels (generic.cu)
+cudaError_t launch_generic(const GenericProgram& p, int grid, int k_begin, int k_end, int call_k0,
+                           cudaStream_t stream);
+int generic_max_coresident_blocks(int device);
+cudaError_t launch_reset(float* arena, const float* pristine, const int64_t* base, const int64_t* pbase,
+                         const int64_t* span, const int32_t* per_batch, int nbuf, int B, cudaStream_t stream);
+cudaError_t launch_probe_transpose(const float* ring, float* out, const int64_t* off, const int32_t* dims,
+                                   int nprobes, int steps, int B, cudaStream_t stream);
+cudaError_t launch_libm_hash_build(unsigned long long* slots, uint32_t mask, int shift, const uint32_t* keys,
+                                   const uint32_t* results, int64_t n, cudaStream_t stream);
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation) throw std::bad_alloc();
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void DevMem::ensure(size_t n) {
+    if (n <= bytes && p) return;
+    release();
+    if (n == 0) n = 16;
+    cuda_check(cudaMalloc(&p, n), "cudaMalloc");
+    bytes = n;
+}
+
+void PinnedMem::ensure(size_t n) {
+    if (n <= bytes && p) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    if (n == 0) n = 16;
+    cuda_check(cudaMallocHost(&p, n), "cudaMallocHost");
+    bytes = n;
+}
+
+// ---------------------------------------------------------------------------
+// libm parity tables
+
+namespace {
+
+std::string library_dir() {
+    Dl_info info{};
+    if (dladdr(reinterpret_cast<void*>(&library_dir), &info) && info.dli_fname) {
+        std::string p = info.dli_fname;
+        auto s = p.find_last_of('/');
+        return s == std::string::npos ? std::string(".") : p.substr(0, s);
+    }
+    return ".";
+}
+
+struct HostTable {
+    std::vector<uint32_t> keys, results;
+};
+
+std::vector<HostTable> load_libm_file() {
+    const char* env = std::getenv("NENG_LIBM_TABLES");
+    std::string path = env ? env : library_dir() + "/data/libm_tables.bin";
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw BuildError("libm parity tables not found at " + path + " (run the package build)");
+    std::vector<char> buf((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    size_t at = 0;
+    auto take = [&](void* dst, size_t n) {
+        if (at + n > buf.size()) throw BuildError("libm parity table file truncated: " + path);
+        std::memcpy(dst, buf.data() + at, n);
+        at += n;
+    };
+    char magic[8];
+    take(magic, 8);
+    if (std::memcmp(magic, "NENGLIBM", 8)) throw BuildError("bad libm parity table file: " + path);
+    uint32_t ver[2];
+    take(ver, 8);
+    std::vector<HostTable> out(3);
+    for (uint32_t t = 0; t < ver[1]; ++t) {
+        uint32_t hdr[2];
+        uint64_t nkb;
+        take(hdr, 8);
+        take(&nkb, 8);
+        if (hdr[0] > 2) throw BuildError("bad libm table index");
+        HostTable& ht = out[hdr[0]];
+        size_t n = hdr[1];
+        ht.keys.resize(n);
+        ht.results.resize(n);
+        const unsigned char* kb = reinterpret_cast<const unsigned char*>(buf.data() + at);
+        size_t kp = 0;
+        uint32_t prev = 0;
+        for (size_t i = 0; i < n; ++i) {
+            uint32_t d = 0;
+            int shift = 0;
+            unsigned char c;
+            do {
+                c = kb[kp++];
+                d |= static_cast<uint32_t>(c & 0x7f) << shift;
+                shift += 7;
+            } while (c & 0x80);
+            prev += d;
+            ht.keys[i] = prev;
+        }
+        at += nkb;
+        const unsigned char* cb = reinterpret_cast<const unsigned char*>(buf.data() + at);
+        at += (n + 3) / 4;
+        // results = host double-then-round +- 1 ulp (code 2: equal)
+        int func = hdr[0] == 0 ? 0 : 1;
+        unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> pool;
+        for (unsigned w = 0; w < nth; ++w)
+            pool.emplace_back([&, w] {
+                for (size_t i = w; i < n; i += nth) {
+                    float x;
+                    std::memcpy(&x, &ht.keys[i], 4);
+                    float r = func == 0 ? static_cast<float>(std::expm1(static_cast<double>(x)))
+                                        : static_cast<float>(std::log1p(static_cast<double>(x)));
+                    uint32_t rb;
+                    std::memcpy(&rb, &r, 4);
+                    int code = (cb[i / 4] >> (2 * (i % 4))) & 3;
+                    ht.results[i] = code == 0 ? rb - 1 : code == 1 ? rb + 1 : rb;
+                }
+            });
+        for (auto& th : pool) th.join();
+    }
+    return out;
+}
+
+struct DeviceLibm {
+    LibmTables tables;
+    std::vector<void*> allocs;
+};
+
+std::mutex g_libm_mu;
+std::map<int, DeviceLibm*> g_libm;  // intentionally leaked for the process lifetime
+
+}  // namespace
+
+const LibmTables& libm_tables(int device) {
+    std::lock_guard<std::mutex> lock(g_libm_mu);
+    auto it = g_libm.find(device);
+    if (it != g_libm.end()) return it->second->tables;
+    std::vector<HostTable> host = load_libm_file();
+    auto* dl = new DeviceLibm();
+    for (int t = 0; t < 3; ++t) {
+        size_t n = host[t].keys.size();
+        int log2cap = 4;
+        while ((size_t{1} << log2cap) < 2 * n + 16) ++log2cap;
+        size_t cap = size_t{1} << log2cap;
+        void* slots = nullptr;
+        cuda_check(cudaMalloc(&slots, cap * sizeof(unsigned long long)), "cudaMalloc libm");
+        cuda_check(cudaMemset(slots, 0, cap * sizeof(unsigned long long)), "cudaMemset libm");
+        void *dk = nullptr, *dr = nullptr;
+        cuda_check(cudaMalloc(&dk, std::max<size_t>(n, 1) * 4), "cudaMalloc libm keys");
+        cuda_check(cudaMalloc(&dr, std::max<size_t>(n, 1) * 4), "cudaMalloc libm results");
+        cuda_check(cudaMemcpy(dk, host[t].keys.data(), n * 4, cudaMemcpyHostToDevice), "libm H2D");
+        cuda_check(cudaMemcpy(dr, host[t].results.data(), n * 4, cudaMemcpyHostToDevice), "libm H2D");
+        cuda_check(launch_libm_hash_build(static_cast<unsigned long long*>(slots), static_cast<uint32_t>(cap - 1),
+                                          32 - log2cap, static_cast<uint32_t*>(dk), static_cast<uint32_t*>(dr),
+                                          static_cast<int64_t>(n), nullptr),
+                   "libm hash build");
+        cuda_check(cudaDeviceSynchronize(), "libm hash build");
+        cudaFree(dk);
+        cudaFree(dr);
+        dl->tables.t[t].slots = static_cast<const unsigned long long*>(slots);
+        dl->tables.t[t].mask = static_cast<uint32_t>(cap - 1);
+        dl->tables.t[t].shift = 32 - log2cap;
+        dl->allocs.push_back(slots);
+    }
+    g_libm[device] = dl;
+    return dl->tables;
+}
+
+// ---------------------------------------------------------------------------
+
+namespace {
+
+std::vector<int> written_positions(const Operator& op) {
+    std::vector<int> w;
+    for (auto [pos, mode] : operand_modes(op))
+        if (mode != AccessMode::Read) w.push_back(pos);
+    return w;
+}
+
+}  // namespace
+
+Engine::Engine(PlannedModel planned, int batch, int unroll, const neng_device_cfg* cfg)
+    : pm_(std::move(planned)), batch_(batch), unroll_(unroll) {
+    // exec.cpp:10-16
+    if (batch_ < 1) throw BuildError("engine batch size must be at least 1");
+    if (unroll_ < 1) throw BuildError("engine unroll factor must be at least 1");
+    if (cfg) {
+        device_ = cfg->device;
+        requested_mode_ = cfg->mode;
+        steps_per_launch_ = cfg->steps_per_launch;
+    }
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    compile();
+}
+
+Engine::~Engine() {
+    fused_.reset();
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+DArg Engine::resolve(const SignalRef& r) const {
+    // resolve (exec.cpp:18-25) in the transposed device layout
+    int bi = pm_.buffers.buffer_of[r.signal];
+    const BufLayout& L = bufs_[bi];
+    int64_t off = (static_cast<int64_t>(pm_.buffers.row_offset[r.signal]) + r.start) * L.epr;
+    DArg a;
+    a.elems = static_cast<int64_t>(r.rows()) * L.epr;
+    a.es = L.per_batch ? batch_ : 1;
+    a.bs = L.per_batch ? 1 : 0;
+    a.base = L.base + off * a.es;
+    return a;
+}
+
+DArg Engine::resolve_full(int sig) const { return resolve({sig, 0, pm_.model.signals[sig].rows()}); }
+
+void Engine::compile() {
+    const BuiltModel& m = pm_.model;
+    const BufferAssignment& ba = pm_.buffers;
+    if (ba.buffer_of.size() != m.signals.size() || ba.row_offset.size() != m.signals.size())
+        throw BuildError("planned model buffer assignment does not cover every signal");
+    for (size_t i = 0; i < m.signals.size(); ++i)
+        if (m.signals[i].id != static_cast<int>(i)) throw StructuralError("signals must be id-indexed");
+    size_t nbuf = ba.buffers.size();
+    bufs_.assign(nbuf, {});
+    // elements per row (exec.cpp:46-51); promoted PES buffers (:54-59)
+    std::vector<char> promoted(nbuf, 0);
+    for (const Operator& op : m.operators)
+        if (op.kind == OpKind::SimPES && op.operands.size() == 3) promoted[ba.buffer_of[op.operands[2].signal]] = 1;
+    int64_t total = 0;
+    std::vector<int64_t> pbase(nbuf);
+    int64_t ptotal = 0;
+    for (size_t bi = 0; bi < nbuf; ++bi) {
+        BufLayout& L = bufs_[bi];
+        L.epr = 1;
+        for (int d : ba.buffers[bi].trailing) L.epr *= d;
+        L.span = static_cast<int64_t>(ba.buffers[bi].rows) * L.epr;
+        L.per_batch = ba.buffers[bi].minibatched || promoted[bi];
+        L.base = total;
+        int64_t n = L.span * (L.per_batch ? batch_ : 1);
+        total += (n + 31) / 32 * 32;  // 128-B aligned bases
+        pbase[bi] = ptotal;
+        ptotal += L.span;
+    }
+    arena_floats_ = total;
+    arena_.ensure(static_cast<size_t>(std::max<int64_t>(total, 1)) * sizeof(float));
+
+    // pristine image (exec.cpp:61-79), fp32
+    std::vector<float> pristine(static_cast<size_t>(std::max<int64_t>(ptotal, 1)), 0.0f);
+    for (const Signal& s : m.signals) {
+        if (s.initial.empty()) continue;
+        int bi = ba.buffer_of[s.id];
+        int64_t at = pbase[bi] + static_cast<int64_t>(ba.row_offset[s.id]) * bufs_[bi].epr;
+        for (size_t k = 0; k < s.initial.size(); ++k) pristine[at + k] = static_cast<float>(s.initial[k]);
+    }
+    pristine_.ensure(pristine.size() * sizeof(float));
+    cuda_check(cudaMemcpy(pristine_.p, pristine.data(), pristine.size() * sizeof(float), cudaMemcpyHostToDevice),
+               "pristine H2D");
+    // reset metadata: base, pbase, span (int64 x3) + per_batch (int32)
+    {
+        std::vector<int64_t> meta(3 * nbuf + 1);
+        std::vector<int32_t> pb(nbuf + 1);
+        for (size_t bi = 0; bi < nbuf; ++bi) {
+            meta[bi] = bufs_[bi].base;
+            meta[nbuf + bi] = pbase[bi];
+            meta[2 * nbuf + bi] = bufs_[bi].span;
+            pb[bi] = bufs_[bi].per_batch;
+        }
+        reset_meta_.ensure(meta.size() * 8 + pb.size() * 4);
+        cuda_check(cudaMemcpy(reset_meta_.p, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice), "meta H2D");
+        cuda_check(cudaMemcpy(static_cast<char*>(reset_meta_.p) + meta.size() * 8, pb.data(), pb.size() * 4,
+                              cudaMemcpyHostToDevice),
+                   "meta H2D");
+    }
+
+    for (const Operator& op : m.operators)
+        if (op.kind == OpKind::SimNeurons &&
+            (op.neuron.kind == NeuronKind::LIF || op.neuron.kind == NeuronKind::LIFRate))
+            needs_libm_ = true;
+
+    compile_generic();
+
+    mode_ = NENG_MODE_GENERIC;
+    if (requested_mode_ != NENG_MODE_GENERIC) {
+        std::string why;
+        fused_ = try_compile_fused(*this, &why);
+        if (fused_)
+            mode_ = NENG_MODE_FUSED;
+        else if (requested_mode_ == NENG_MODE_FUSED)
+            throw BuildError("fused pipeline unavailable for this model: " + why);
+    }
+    reset();
+}
+
+void Engine::compile_generic() {
+    const BuiltModel& m = pm_.model;
+    std::unordered_map<int, const Operator*> by_id;
+    for (const Operator& op : m.operators) by_id.emplace(op.id, &op);
+
+    std::vector<DGroup> groups;
+    std::vector<DMember> members;
+    std::vector<DTile> tiles;
+    std::vector<float> values;
+    int max_tiles = 1;
+    for (const OpGroup& og : pm_.plan) {
+        if (og.members.empty()) throw BuildError("plan has an empty group");
+        auto fit = by_id.find(og.members[0]);
+        if (fit == by_id.end())
+            throw BuildError("plan names operator " + std::to_string(og.members[0]) + " which does not exist");
+        const Operator& first = *fit->second;
+        DGroup g;
+        g.kind = static_cast<int32_t>(first.kind);
+        if (first.kind == OpKind::Copy && first.inc) g.flags |= GF_INC;
+        g.dt = static_cast<float>(m.dt);  // Instr::dt = (T)model.dt (exec.cpp:88)
+        if (first.kind == OpKind::SimNeurons) {
+            g.neuron = static_cast<int32_t>(first.neuron.kind);
+            g.tau_rc = static_cast<float>(first.neuron.tau_rc);
+            g.tau_ref = static_cast<float>(first.neuron.tau_ref);
+            g.amplitude = static_cast<float>(first.neuron.amplitude);
+        } else if (first.kind == OpKind::SimProcess) {
+            double a = 0.0, b = 1.0;  // lowpass_coefficients (neuron_math.hpp:33-37)
+            if (first.tau > 0.0) {
+                a = std::exp(-m.dt / first.tau);
+                b = 1.0 - a;
+            }
+            g.tau_a = static_cast<float>(a);
+            g.tau_b = static_cast<float>(b);
+            if (first.operands.size() >= 3) g.flags |= GF_HAS_STATE;
+        }
+        auto modes = operand_modes(first);
+        auto wpos = written_positions(first);
+        // per_batch (exec.cpp:122-125) from member 0's buffers
+        int wpb = 0, wshared = 0;
+        for (int p : wpos) {
+            int bi = pm_.buffers.buffer_of[first.operands[p].signal];
+            if (bufs_[bi].per_batch)
+                wpb = 1;
+            else
+                wshared = 1;
+        }
+        if (wpb) g.flags |= GF_PER_BATCH;
+        g.copies = wpb ? batch_ : 1;
+        if (wpb && wshared && batch_ > 1) g.flags |= GF_SERIAL_B;
+        g.member_begin = static_cast<int32_t>(members.size());
+        g.tile_begin = static_cast<int32_t>(tiles.size());
+        for (OpId id : og.members) {
+            auto it = by_id.find(id);
+            if (it == by_id.end())
+                throw BuildError("plan names operator " + std::to_string(id) + " which does not exist");
+            const Operator& op = *it->second;
+            if (op.kind != first.kind) throw BuildError("plan group mixes operator kinds");
+            DMember dm;
+            for (size_t p = 0; p < op.operands.size() && p < 4; ++p) dm.a[p] = resolve(op.operands[p]);
+            if (op.kind == OpKind::Reset) {
+                dm.value_at = static_cast<int64_t>(values.size());
+                for (double v : op.value) values.push_back(static_cast<float>(v));
+            }
+            switch (op.kind) {
+                case OpKind::Reset: dm.items = dm.a[0].elems; break;
+                case OpKind::Copy: dm.items = dm.a[0].elems; break;
+                case OpKind::ElementwiseInc:
+                    dm.items = dm.a[1].elems;
+                    if (dm.a[0].elems == 1) dm.flags |= MF_SCALAR_A;
+                    break;
+                case OpKind::DotInc: dm.items = dm.a[2].elems; break;
+                case OpKind::SimNeurons: dm.items = dm.a[0].elems; break;
+                case OpKind::SimProcess: dm.items = dm.a[0].elems; break;
+                case OpKind::SimPES:
+                    dm.items = dm.a[0].elems * dm.a[1].elems;
+                    dm.pes_scale = static_cast<float>(first.learning_rate * m.dt /
+                                                      static_cast<double>(dm.a[0].elems));
+                    break;
+                case OpKind::TimeUpdate: dm.items = 1; break;
+            }
+            // self-aliasing with an offset -> reference loop order (GF_SERIAL_ALL)
+            auto wp = written_positions(op);
+            for (int p : wp)
+                for (size_t q = 0; q < op.operands.size(); ++q) {
+                    if (static_cast<int>(q) == p) continue;
+                    int bp = pm_.buffers.buffer_of[op.operands[p].signal];
+                    int bq = pm_.buffers.buffer_of[op.operands[q].signal];
+                    if (bp != bq) continue;
+                    const DArg &A = dm.a[p], &Q = dm.a[q];
+                    bool overlap = A.base < Q.base + Q.elems * A.es && Q.base < A.base + A.elems * A.es;
+                    if (!overlap) continue;
+                    bool elementwise_same = A.base == Q.base && A.elems == Q.elems &&
+                                            !(op.kind == OpKind::ElementwiseInc && (dm.flags & MF_SCALAR_A));
+                    if (!elementwise_same) g.flags |= GF_SERIAL_ALL;
+                }
+            int64_t total_items = dm.items * g.copies;
+            int mi = static_cast<int>(members.size());
+            for (int64_t s = 0; s < total_items; s += kTile)
+                tiles.push_back({mi, static_cast<int32_t>(s), static_cast<int32_t>(std::min<int64_t>(kTile, total_items - s))});
+            if (total_items > (int64_t{1} << 30)) throw BuildError("group member too large for the generic path");
+            members.push_back(dm);
+        }
+        g.n_members = static_cast<int32_t>(members.size()) - g.member_begin;
+        g.n_tiles = static_cast<int32_t>(tiles.size()) - g.tile_begin;
+        g.flags |= GF_BARRIER;
+        if (!(g.flags & (GF_SERIAL_ALL | GF_SERIAL_B))) max_tiles = std::max(max_tiles, g.n_tiles);
+        groups.push_back(g);
+    }
+
+    // feeds / probes (exec.cpp:150-159)
+    feeds_.clear();
+    for (const FeedSlot& fs : m.feed_slots) {
+        DFeed f;
+        f.dst = resolve_full(fs.signal);
+        f.dim = fs.dim;
+        f.copies = bufs_[pm_.buffers.buffer_of[fs.signal]].per_batch ? batch_ : 1;
+        feeds_.push_back(f);
+    }
+    probes_.clear();
+    int64_t roff = 0;
+    for (const ProbeRegistration& p : m.probes) {
+        DProbe q;
+        q.src = resolve_full(p.signal);
+        q.dim = static_cast<int32_t>(m.signals[p.signal].size());
+        q.per_batch = bufs_[pm_.buffers.buffer_of[p.signal]].per_batch;
+        q.ring_off = roff;
+        roff += q.dim;  // scaled by n_steps*B per call
+        probes_.push_back(q);
+    }
+
+    auto upload = [](DevMem& dst, const void* src, size_t bytes) {
+        dst.ensure(std::max<size_t>(bytes, 16));
+        if (bytes) cuda_check(cudaMemcpy(dst.p, src, bytes, cudaMemcpyHostToDevice), "program H2D");
+    };
+    upload(d_groups_, groups.data(), groups.size() * sizeof(DGroup));
+    upload(d_members_, members.data(), members.size() * sizeof(DMember));
+    upload(d_tiles_, tiles.data(), tiles.size() * sizeof(DTile));
+    upload(d_values_, values.data(), values.size() * sizeof(float));
+
+    prog_ = GenericProgram{};
+    prog_.arena = arena_.as<float>();
+    prog_.groups = d_groups_.as<DGroup>();
+    prog_.members = d_members_.as<DMember>();
+    prog_.tiles = d_tiles_.as<DTile>();
+    prog_.values = d_values_.as<float>();
+    prog_.n_groups = static_cast<int32_t>(groups.size());
+    prog_.n_feeds = static_cast<int32_t>(feeds_.size());
+    prog_.n_probes = static_cast<int32_t>(probes_.size());
+    prog_.batch = batch_;
+    if (needs_libm_) prog_.libm = libm_tables(device_);
+
+    int maxco = generic_max_coresident_blocks(device_);
+    grid_ = std::max(1, std::min(maxco, max_tiles));
+    // tiny programs: one CTA, block-level barriers only
+    if (max_tiles <= 2) grid_ = 1;
+}
+
+void Engine::reset() {
+    // exec.cpp:164-174
+    size_t nbuf = bufs_.size();
+    const int64_t* meta = reset_meta_.as<int64_t>();
+    const int32_t* pb = reinterpret_cast<const int32_t*>(reset_meta_.as<char>() + (3 * nbuf + 1) * 8);
+    cuda_check(launch_reset(arena_.as<float>(), pristine_.as<float>(), meta, meta + nbuf, meta + 2 * nbuf, pb,
+                            static_cast<int>(nbuf), batch_, stream_),
+               "reset");
+    if (fused_) fused_->load_from_arena(stream_);
+    cuda_check(cudaStreamSynchronize(stream_), "reset");
+    steps_done_ = 0;
+}
+
+void Engine::validate_feeds(int n_feeds, const neng_feed* feeds, int n_steps) const {
+    // validate_feeds (model.hpp:62-83); FeedData iterates in node-id order
+    const BuiltModel& m = pm_.model;
+    std::vector<const neng_feed*> order;
+    for (int i = 0; i < n_feeds; ++i) order.push_back(&feeds[i]);
+    std::stable_sort(order.begin(), order.end(),
+                     [](const neng_feed* a, const neng_feed* b) { return a->node_id < b->node_id; });
+    for (const neng_feed* t : order) {
+        const FeedSlot* slot = nullptr;
+        for (const FeedSlot& s : m.feed_slots)
+            if (s.node_id == t->node_id) slot = &s;
+        if (!slot) throw RunError("feed for unknown node " + std::to_string(t->node_id));
+        if (t->batch != batch_ || t->steps < n_steps || t->dim != slot->dim) {
+            std::ostringstream os;
+            os << "feed for node " << t->node_id << " ('" << slot->label << "') has shape (" << t->batch << ", "
+               << t->steps << ", " << t->dim << "), expected (" << batch_ << ", >=" << n_steps << ", " << slot->dim
+               << ")";
+            throw RunError(os.str());
+        }
+        if (!t->data && static_cast<int64_t>(t->batch) * t->steps * t->dim > 0)
+            throw InvalidArgument("feed data pointer is null");
+    }
+    for (const FeedSlot& s : m.feed_slots) {
+        bool found = false;
+        for (int i = 0; i < n_feeds; ++i) found |= feeds[i].node_id == s.node_id;
+        if (!s.has_default && !found)
+            throw RunError("node " + std::to_string(s.node_id) + " ('" + s.label +
+                           "') has no default output and no feed was supplied");
+    }
+}
+
+void Engine::launch_steps(int n_steps, const float* d_feed_data, const std::vector<int>& present, float* d_ring,
+                          cudaStream_t stream) {
+    last_launches_ = 0;
+    std::vector<int64_t> feed_off(feeds_.size()), ring_off(probes_.size());
+    int64_t at = 0;
+    for (size_t f = 0; f < feeds_.size(); ++f) {
+        feed_off[f] = at;
+        if (present[f]) at += static_cast<int64_t>(n_steps) * feeds_[f].dim * batch_;
+    }
+    at = 0;
+    for (size_t q = 0; q < probes_.size(); ++q) {
+        ring_off[q] = at;
+        at += static_cast<int64_t>(n_steps) * probes_[q].dim * batch_;
+    }
+    if (fused_) {
+        last_launches_ = fused_->run(n_steps, d_feed_data, feed_off.data(), present.data(), d_ring, ring_off.data(),
+                                     stream);
+        return;
+    }
+    // refresh per-call feed/probe descriptors
+    bool any = false;
+    for (size_t f = 0; f < feeds_.size(); ++f) {
+        feeds_[f].present = present[f];
+        feeds_[f].data_off = feed_off[f];
+        any |= present[f] != 0;
+    }
+    for (size_t q = 0; q < probes_.size(); ++q) probes_[q].ring_off = ring_off[q];
+    size_t fb = feeds_.size() * sizeof(DFeed), pbytes = probes_.size() * sizeof(DProbe);
+    d_feeds_.ensure(std::max<size_t>(fb, 16));
+    d_probes_.ensure(std::max<size_t>(pbytes, 16));
+    if (fb) cuda_check(cudaMemcpyAsync(d_feeds_.p, feeds_.data(), fb, cudaMemcpyHostToDevice, stream), "feeds H2D");
+    if (pbytes)
+        cuda_check(cudaMemcpyAsync(d_probes_.p, probes_.data(), pbytes, cudaMemcpyHostToDevice, stream), "probes H2D");
+    GenericProgram p = prog_;
+    p.feeds = d_feeds_.as<DFeed>();
+    p.probes = d_probes_.as<DProbe>();
+    p.any_feed = any ? 1 : 0;
+    p.feed_data = d_feed_data;
+    p.ring = d_ring;
+    p.call_steps = n_steps;
+    int K = steps_per_launch_ > 0 ? steps_per_launch_ : n_steps;
+    for (int k = 0; k < n_steps; k += K) {
+        cuda_check(launch_generic(p, grid_, k, std::min(n_steps, k + K), 0, stream), "generic kernel launch");
+        ++last_launches_;
+    }
+    // the descriptor upload must finish before the host vectors change again
+    cuda_check(cudaStreamSynchronize(stream), "generic run");
+}
+
+void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probes_out) {
+    // exec.cpp:340-366
+    if (n_steps <= 0) throw RunError("n_steps must be positive");
+    if (n_feeds < 0 || (n_feeds > 0 && !feeds)) throw InvalidArgument("bad feed array");
+    validate_feeds(n_feeds, feeds, n_steps);
+    const BuiltModel& m = pm_.model;
+    const int B = batch_;
+    // stage feeds as f32 [slot][step][dim][B] (the write_feeds cast, exec.cpp:323)
+    std::vector<int> present(feeds_.size(), 0);
+    std::vector<const neng_feed*> src(feeds_.size(), nullptr);
+    int64_t feed_floats = 0;
+    for (size_t f = 0; f < m.feed_slots.size(); ++f) {
+        for (int i = 0; i < n_feeds; ++i)
+            if (feeds[i].node_id == m.feed_slots[f].node_id) src[f] = &feeds[i];
+        if (src[f]) {
+            present[f] = 1;
+            feed_floats += static_cast<int64_t>(n_steps) * feeds_[f].dim * B;
+        }
+    }
+    feed_stage_.ensure(static_cast<size_t>(std::max<int64_t>(feed_floats, 1)) * sizeof(float));
+    float* stage = feed_stage_.as<float>();
+    int64_t at = 0;
+    for (size_t f = 0; f < feeds_.size(); ++f) {
+        if (!present[f]) continue;
+        const neng_feed* t = src[f];
+        const int dim = feeds_[f].dim;
+        for (int s = 0; s < n_steps; ++s)
+            for (int d = 0; d < dim; ++d) {
+                float* row = stage + at + (static_cast<int64_t>(s) * dim + d) * B;
+                for (int b = 0; b < B; ++b)
+                    row[b] = static_cast<float>(t->data[(static_cast<int64_t>(b) * t->steps + s) * t->dim + d]);
+            }
+        at += static_cast<int64_t>(n_steps) * dim * B;
+    }
+    feed_buf_.ensure(static_cast<size_t>(std::max<int64_t>(feed_floats, 1)) * sizeof(float));
+    if (feed_floats)
+        cuda_check(cudaMemcpyAsync(feed_buf_.p, stage, feed_floats * sizeof(float), cudaMemcpyHostToDevice, stream_),
+                   "feed H2D");
+    int64_t ring_floats = 0;
+    for (const DProbe& q : probes_) ring_floats += static_cast<int64_t>(n_steps) * q.dim * B;
+    ring_.ensure(static_cast<size_t>(std::max<int64_t>(ring_floats, 1)) * sizeof(float));
+
+    launch_steps(n_steps, feed_buf_.as<float>(), present, ring_.as<float>(), stream_);
+
+    if (ring_floats) {
+        // ring [probe][step][dim][B] -> [probe][B][step][dim], D2H, widen to f64
+        std::vector<int64_t> off(probes_.size());
+        std::vector<int32_t> dims(probes_.size());
+        int64_t o = 0;
+        for (size_t q = 0; q < probes_.size(); ++q) {
+            off[q] = o;
+            dims[q] = probes_[q].dim;
+            o += static_cast<int64_t>(n_steps) * probes_[q].dim * B;
+        }
+        probe_meta_.ensure(probes_.size() * 12 + 16);
+        cuda_check(cudaMemcpyAsync(probe_meta_.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice, stream_),
+                   "probe meta");
+        cuda_check(cudaMemcpyAsync(probe_meta_.as<char>() + off.size() * 8, dims.data(), dims.size() * 4,
+                                   cudaMemcpyHostToDevice, stream_),
+                   "probe meta");
+        probe_out_.ensure(ring_floats * sizeof(float));
+        cuda_check(launch_probe_transpose(ring_.as<float>(), probe_out_.as<float>(), probe_meta_.as<int64_t>(),
+                                          reinterpret_cast<int32_t*>(probe_meta_.as<char>() + off.size() * 8),
+                                          static_cast<int>(probes_.size()), n_steps, B, stream_),
+                   "probe transpose");
+        probe_stage_.ensure(ring_floats * sizeof(float));
+        cuda_check(cudaMemcpyAsync(probe_stage_.p, probe_out_.p, ring_floats * sizeof(float), cudaMemcpyDeviceToHost,
+                                   stream_),
+                   "probe D2H");
+        cuda_check(cudaStreamSynchronize(stream_), "run");
+        if (probes_out) {
+            const float* ps = probe_stage_.as<float>();
+            for (int64_t i = 0; i < ring_floats; ++i) probes_out[i] = static_cast<double>(ps[i]);
+        }
+    } else {
+        cuda_check(cudaStreamSynchronize(stream_), "run");
+    }
+    steps_done_ += n_steps;
+}
+
+void Engine::run_device(int n_steps, const float* const* d_feeds, float* const* d_probes, cudaStream_t stream) {
+    if (n_steps <= 0) throw RunError("n_steps must be positive");
+    if (!stream) stream = stream_;
+    const BuiltModel& m = pm_.model;
+    // feeds: per slot pointer -> gather offsets relative to the first present block
+    std::vector<int> present(feeds_.size(), 0);
+    for (size_t f = 0; f < m.feed_slots.size(); ++f) {
+        present[f] = d_feeds && d_feeds[f] ? 1 : 0;
+        if (!present[f] && !m.feed_slots[f].has_default)
+            throw RunError("node " + std::to_string(m.feed_slots[f].node_id) + " ('" + m.feed_slots[f].label +
+                           "') has no default output and no feed was supplied");
+    }
+    // the device program addresses feed and probe blocks by offset from one
+    // base; require the caller's blocks to be packed in model order
+    const float* base = nullptr;
+    int64_t expect = 0;
+    for (size_t f = 0; f < feeds_.size(); ++f) {
+        if (!present[f]) continue;
+        if (!base) base = d_feeds[f];
+        if (d_feeds[f] != base + expect) throw InvalidArgument("run_device: feed blocks must be packed in slot order");
+        expect += static_cast<int64_t>(n_steps) * feeds_[f].dim * batch_;
+    }
+    float* ring = nullptr;
+    int64_t rexp = 0;
+    for (size_t q = 0; q < probes_.size(); ++q) {
+        if (!d_probes || !d_probes[q]) throw InvalidArgument("run_device: every probe needs an output block");
+        if (!ring) ring = d_probes[q];
+        if (d_probes[q] != ring + rexp) throw InvalidArgument("run_device: probe blocks must be packed in order");
+        rexp += static_cast<int64_t>(n_steps) * probes_[q].dim * batch_;
+    }
+    launch_steps(n_steps, base, present, ring, stream);
+    steps_done_ += n_steps;
+}
+
+void Engine::synchronize() { cuda_check(cudaStreamSynchronize(stream_), "synchronize"); }
+
+std::vector<double> Engine::read_signal(int sig, int batch_index) const {
+    // exec.cpp:368-377
+    if (sig < 0 || sig >= static_cast<int>(pm_.model.signals.size())) throw RunError("read_signal: no such signal");
+    if (batch_index < 0 || batch_index >= batch_) throw RunError("read_signal: batch index out of range");
+    if (fused_) fused_->materialize(stream_);
+    DArg a = resolve_full(sig);
+    std::vector<float> tmp(static_cast<size_t>(std::max<int64_t>(a.elems, 1)));
+    int b = a.bs ? batch_index : 0;
+    if (a.elems) {
+        const float* src = arena_.as<float>() + a.base + static_cast<int64_t>(b) * a.bs;
+        cuda_check(cudaMemcpy2DAsync(tmp.data(), sizeof(float), src, static_cast<size_t>(a.es) * sizeof(float),
+                                     sizeof(float), static_cast<size_t>(a.elems), cudaMemcpyDeviceToHost, stream_),
+                   "read_signal D2H");
+        cuda_check(cudaStreamSynchronize(stream_), "read_signal");
+    }
+    return std::vector<double>(tmp.begin(), tmp.begin() + a.elems);
+}
+
+int Engine::buffer_storage(int buffer) const {
+    if (buffer < 0 || buffer >= static_cast<int>(bufs_.size())) throw RunError("buffer_storage: no such buffer");
+    return bufs_[buffer].per_batch ? NENG_STORAGE_PER_BATCH : NENG_STORAGE_SHARED;
+}
+
+}  // namespace nengb

@@ -1,0 +1,127 @@
+// engine.hpp — the B200 engine behind include/neng_gpu.h.  Mirrors
+// neng::EngineCore<float> (proj/include/nengine/exec.hpp:18-120): it owns the
+// planned model, compiles it once into a device program and device storage,
+// and steps it with persistent kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../kernels/program.hpp"
+#include "host_ir.hpp"
+
+namespace nengb {
+
+struct FusedPlan;  // fused ensemble pipeline (fused.hpp)
+
+// Device buffer that frees itself.
+struct DevMem {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevMem() = default;
+    DevMem(const DevMem&) = delete;
+    DevMem& operator=(const DevMem&) = delete;
+    ~DevMem() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void ensure(size_t n);  // grow-only
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct PinnedMem {
+    void* p = nullptr;
+    size_t bytes = 0;
+    PinnedMem() = default;
+    PinnedMem(const PinnedMem&) = delete;
+    PinnedMem& operator=(const PinnedMem&) = delete;
+    ~PinnedMem() {
+        if (p) cudaFreeHost(p);
+    }
+    void ensure(size_t n);
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+/// Singleton per device: glibc-parity hash tables for expm1f/log1pf.
+const LibmTables& libm_tables(int device);
+
+class Engine {
+  public:
+    Engine(PlannedModel planned, int batch, int unroll, const neng_device_cfg* cfg);
+    ~Engine();
+
+    void run(int n_steps, int n_feeds, const neng_feed* feeds, double* probes_out);
+    void run_device(int n_steps, const float* const* d_feeds, float* const* d_probes, cudaStream_t stream);
+    void reset();
+    std::vector<double> read_signal(int sig, int batch_index) const;
+    int buffer_storage(int buffer) const;
+    void synchronize();
+
+    int batch() const { return batch_; }
+    int unroll() const { return unroll_; }
+    int steps_completed() const { return steps_done_; }
+    int mode() const { return mode_; }
+    int64_t last_launches() const { return last_launches_; }
+    const PlannedModel& planned() const { return pm_; }
+    int num_probes() const { return static_cast<int>(pm_.model.probes.size()); }
+    int probe_dim(int i) const { return static_cast<int>(pm_.model.signals[pm_.model.probes[i].signal].size()); }
+
+    std::string last_error;
+
+    // layout (public for the fused compiler)
+    struct BufLayout {
+        int64_t epr = 1, span = 0, base = 0;
+        int per_batch = 0;
+    };
+    DArg resolve(const SignalRef& r) const;
+    DArg resolve_full(int sig) const;
+    const std::vector<BufLayout>& layout() const { return bufs_; }
+    float* arena() const { return arena_.as<float>(); }
+    cudaStream_t stream() const { return stream_; }
+
+  private:
+    void compile();
+    void compile_generic();
+    void validate_feeds(int n_feeds, const neng_feed* feeds, int n_steps) const;
+    void launch_steps(int n_steps, const float* d_feed_data, const std::vector<int>& present, float* d_ring,
+                      cudaStream_t stream);
+
+    PlannedModel pm_;
+    int batch_, unroll_, steps_done_ = 0;
+    int device_ = 0, mode_ = NENG_MODE_GENERIC, requested_mode_ = NENG_MODE_AUTO, steps_per_launch_ = 0;
+    cudaStream_t stream_ = nullptr;
+    int64_t last_launches_ = 0;
+
+    std::vector<BufLayout> bufs_;
+    DevMem arena_, pristine_, reset_meta_;
+    int64_t arena_floats_ = 0;
+
+    // generic program
+    GenericProgram prog_;
+    DevMem d_groups_, d_members_, d_tiles_, d_values_, d_feeds_, d_probes_;
+    std::vector<DFeed> feeds_;
+    std::vector<DProbe> probes_;
+    int grid_ = 1;
+    bool needs_libm_ = false;
+
+    std::unique_ptr<FusedPlan> fused_;
+
+    // per-call scratch
+    DevMem feed_buf_, ring_, probe_out_, probe_meta_;
+    PinnedMem feed_stage_, probe_stage_;
+};
+
+}  // namespace nengb

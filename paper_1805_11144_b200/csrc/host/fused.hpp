@@ -1,0 +1,35 @@
+// fused.hpp — the fused ensemble pipeline (see fused_compile.cpp).
+#pragma once
+
+#include <memory>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "../kernels/program.hpp"
+
+namespace nengb {
+
+class Engine;
+
+/// A compiled fused program: recognises the ensemble/connection structure of
+/// the planned model and advances whole steps with one grid barrier each.
+struct FusedPlan {
+    virtual ~FusedPlan() = default;
+    /// Advance n_steps; feed data [slot][n][dim][B] f32 (slots absent -> null
+    /// entries), probe ring [probe][n][dim][B].  Returns kernel launches.
+    virtual int64_t run(int n_steps, const float* d_feed_data, const int64_t* feed_off, const int* present,
+                        float* d_ring, const int64_t* ring_off, cudaStream_t stream) = 0;
+    /// Write every signal the fused kernel keeps on-chip back to the arena so
+    /// the arena holds the reference's state (read_signal, mode switches).
+    virtual void materialize(cudaStream_t stream) = 0;
+    /// Re-derive fused-private state from the arena (after reset).
+    virtual void load_from_arena(cudaStream_t stream) = 0;
+    virtual std::string describe() const = 0;
+};
+
+/// Returns nullptr (and a reason) when the model is not an ensemble network
+/// the fused pipeline reproduces exactly.
+std::unique_ptr<FusedPlan> try_compile_fused(Engine& e, std::string* why);
+
+}  // namespace nengb

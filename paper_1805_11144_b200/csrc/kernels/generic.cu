@@ -1,0 +1,360 @@
+// generic.cu — the persistent cooperative interpreter: advances K timesteps
+// per launch over ANY planned model, one pass per plan group with a grid
+// barrier between dependent passes (the reference's run loop, exec.cpp:340-366,
+// with each Instr's `for b < copies: exec(ins, b)` flattened into one parallel
+// pass over (member, element, batch copy)).
+//
+// Exactness argument: members of a group never overlap in writes and never
+// read what another member of the same group writes (every write/read pair on
+// overlapping rows is a dependency edge, ir.cpp:351-360, and validate_plan
+// puts edge endpoints in different groups, passes.cpp:279-305), so any
+// parallel order inside a pass is exact.  Two cases are not data-parallel and
+// run in the reference's loop order instead:
+//   GF_SERIAL_ALL  a member whose written operand overlaps another operand of
+//                  the same member at a different offset (e.g. Copy(s[0:3] ->
+//                  s[1:4], inc) cascades); one thread, exact reference loops.
+//   GF_SERIAL_B    a per-batch group that writes shared storage: copies b run
+//                  in order, elements in parallel within each b.
+// Every float operation is the reference's (no FMA: -fmad=false; IEEE div).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "libm.cuh"
+#include "neng_gpu.h"
+#include "program.hpp"
+
+namespace cg = cooperative_groups;
+
+namespace nengb {
+
+__device__ __forceinline__ float* at(const GenericProgram& p, const DArg& a, int64_t e, int b) {
+    return p.arena + a.base + e * a.es + static_cast<int64_t>(b) * a.bs;
+}
+
+// One work item of a data-parallel group. local indexes the member's
+// per-copy work (element, row, or (row, col) for PES).
+__device__ __forceinline__ void exec_item(const GenericProgram& p, const DGroup& g, const DMember& m,
+                                          int64_t local, int b) {
+    switch (g.kind) {
+        case 0: {  // Reset (exec.cpp:179-188)
+            *at(p, m.a[0], local, b) = p.values[m.value_at + local];
+            break;
+        }
+        case 1: {  // Copy (exec.cpp:189-210)
+            float s = *at(p, m.a[0], local, b);
+            float* d = at(p, m.a[1], local, b);
+            if (g.flags & GF_INC)
+                *d = *d + s;
+            else
+                *d = s;
+            break;
+        }
+        case 2: {  // ElementwiseInc (exec.cpp:211-225)
+            float a = (m.flags & MF_SCALAR_A) ? *at(p, m.a[0], 0, b) : *at(p, m.a[0], local, b);
+            float x = *at(p, m.a[1], local, b);
+            float* y = at(p, m.a[2], local, b);
+            *y = *y + a * x;
+            break;
+        }
+        case 3: {  // DotInc (exec.cpp:226-240): acc = 0; acc += A[r,k]*x[k] in k order; y[r] += acc
+            const int64_t n = m.a[1].elems;
+            const float* arow = at(p, m.a[0], local * n, b);
+            const int32_t aes = m.a[0].es;
+            const float* x = at(p, m.a[1], 0, b);
+            const int32_t xes = m.a[1].es;
+            float acc = 0.0f;
+            for (int64_t k = 0; k < n; ++k) acc = acc + arow[k * aes] * x[k * xes];
+            float* y = at(p, m.a[2], local, b);
+            *y = *y + acc;
+            break;
+        }
+        case 4: {  // SimNeurons (exec.cpp:241-266)
+            float j = *at(p, m.a[0], local, b);
+            float* out = at(p, m.a[1], local, b);
+            if (g.neuron == NENG_NEURON_LIF) {
+                float* vp = at(p, m.a[2], local, b);
+                float* rp = at(p, m.a[3], local, b);
+                float v = *vp, r = *rp;
+                float o = lif_spike_step(j, v, r, g.dt, g.tau_rc, g.tau_ref, g.amplitude, p.libm);
+                *out = o;  // write order of exec.cpp:252-254 (last write wins on aliasing)
+                *vp = v;
+                *rp = r;
+            } else if (g.neuron == NENG_NEURON_LIF_RATE) {
+                *out = lif_rate_out(j, g.tau_rc, g.tau_ref, g.amplitude, p.libm);
+            } else {
+                *out = relu_out(j, g.amplitude);
+            }
+            break;
+        }
+        case 5: {  // SimProcess (exec.cpp:267-284)
+            float in = *at(p, m.a[0], local, b);
+            float* out = at(p, m.a[1], local, b);
+            if (g.flags & GF_HAS_STATE) {
+                float* st = at(p, m.a[2], local, b);
+                float f = g.tau_a * *st + g.tau_b * in;  // lowpass_step
+                *st = f;
+                *out = f;
+            } else {
+                *out = in;
+            }
+            break;
+        }
+        case 6: {  // SimPES (exec.cpp:285-299): w[r,k] -= (scale*err[r]) * act[k]
+            const int64_t n = m.a[0].elems;
+            int64_t r = local / n, k = local - r * n;
+            float row_scale = m.pes_scale * *at(p, m.a[1], r, b);
+            float* w = at(p, m.a[2], local, b);
+            *w = *w - row_scale * *at(p, m.a[0], k, b);
+            break;
+        }
+        case 7: {  // TimeUpdate (exec.cpp:300-309)
+            float* step = at(p, m.a[0], 0, b);
+            float* time = at(p, m.a[1], 0, b);
+            float next = *step + 1.0f;
+            *step = next;
+            *time = next * g.dt;
+            break;
+        }
+    }
+}
+
+// Reference loop order for one member and one copy b (GF_SERIAL_ALL).
+__device__ void exec_member_serial(const GenericProgram& p, const DGroup& g, const DMember& m, int b) {
+    switch (g.kind) {
+        case 1: {  // Copy: inc cascades forward; plain copy is std::copy == memmove
+            const int64_t n = m.a[0].elems;
+            if (g.flags & GF_INC) {
+                for (int64_t i = 0; i < n; ++i) {
+                    float s = *at(p, m.a[0], i, b);
+                    float* d = at(p, m.a[1], i, b);
+                    *d = *d + s;
+                }
+            } else if (m.a[1].base > m.a[0].base) {
+                for (int64_t i = n - 1; i >= 0; --i) *at(p, m.a[1], i, b) = *at(p, m.a[0], i, b);
+            } else {
+                for (int64_t i = 0; i < n; ++i) *at(p, m.a[1], i, b) = *at(p, m.a[0], i, b);
+            }
+            break;
+        }
+        case 2: {  // ElementwiseInc: scalar read once before the loop
+            const int64_t n = m.a[1].elems;
+            if (m.flags & MF_SCALAR_A) {
+                float s = *at(p, m.a[0], 0, b);
+                for (int64_t i = 0; i < n; ++i) {
+                    float* y = at(p, m.a[2], i, b);
+                    *y = *y + s * *at(p, m.a[1], i, b);
+                }
+            } else {
+                for (int64_t i = 0; i < n; ++i) {
+                    float* y = at(p, m.a[2], i, b);
+                    *y = *y + *at(p, m.a[0], i, b) * *at(p, m.a[1], i, b);
+                }
+            }
+            break;
+        }
+        case 5: {  // SimProcess
+            const int64_t n = m.a[0].elems;
+            if (g.flags & GF_HAS_STATE) {
+                for (int64_t i = 0; i < n; ++i) {
+                    float* st = at(p, m.a[2], i, b);
+                    float f = g.tau_a * *st + g.tau_b * *at(p, m.a[0], i, b);
+                    *st = f;
+                    *at(p, m.a[1], i, b) = f;
+                }
+            } else if (m.a[1].base > m.a[0].base) {
+                for (int64_t i = n - 1; i >= 0; --i) *at(p, m.a[1], i, b) = *at(p, m.a[0], i, b);
+            } else {
+                for (int64_t i = 0; i < n; ++i) *at(p, m.a[1], i, b) = *at(p, m.a[0], i, b);
+            }
+            break;
+        }
+        default: {  // element-sequential kinds: one item after another, in order
+            int64_t items = m.items;
+            for (int64_t i = 0; i < items; ++i) exec_item(p, g, m, i, b);
+            break;
+        }
+    }
+}
+
+__device__ __forceinline__ void grid_sync(cg::grid_group& grid) {
+    if (gridDim.x == 1)
+        __syncthreads();
+    else
+        grid.sync();
+}
+
+__global__ void __launch_bounds__(kTile) generic_run_kernel(GenericProgram p, int k_begin, int k_end,
+                                                            int call_k0) {
+    cg::grid_group grid = cg::this_grid();
+    const int B = p.batch;
+    for (int k = k_begin; k < k_end; ++k) {
+        const int ks = k - call_k0;  // step index within this run() call
+        // write_feeds (exec.cpp:313-326): per-batch slots take row b, shared slots row 0
+        if (p.any_feed) {
+            for (int f = 0; f < p.n_feeds; ++f) {
+                const DFeed& fd = p.feeds[f];
+                if (!fd.present) continue;
+                const int64_t n = static_cast<int64_t>(fd.dim) * fd.copies;
+                const float* src = p.feed_data + fd.data_off + static_cast<int64_t>(ks) * fd.dim * B;
+                for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+                    int64_t d = i / fd.copies;
+                    int b = static_cast<int>(i - d * fd.copies);
+                    *at(p, fd.dst, d, b) = src[d * B + b];
+                }
+            }
+            grid_sync(grid);
+        }
+        for (int gi = 0; gi < p.n_groups; ++gi) {
+            const DGroup g = p.groups[gi];
+            if (g.flags & GF_SERIAL_ALL) {
+                if (blockIdx.x == 0 && threadIdx.x == 0)
+                    for (int b = 0; b < g.copies; ++b)
+                        for (int mi = 0; mi < g.n_members; ++mi)
+                            exec_member_serial(p, g, p.members[g.member_begin + mi], b);
+            } else if (g.flags & GF_SERIAL_B) {
+                if (blockIdx.x == 0)
+                    for (int b = 0; b < g.copies; ++b) {
+                        for (int t = 0; t < g.n_tiles; ++t) {
+                            const DTile tl = p.tiles[g.tile_begin + t];
+                            const DMember& m = p.members[tl.member];
+                            int i = tl.start + threadIdx.x;
+                            if (threadIdx.x < tl.count && i % g.copies == b) exec_item(p, g, m, i / g.copies, b);
+                        }
+                        __syncthreads();
+                    }
+            } else {
+                for (int t = blockIdx.x; t < g.n_tiles; t += gridDim.x) {
+                    const DTile tl = p.tiles[g.tile_begin + t];
+                    if (threadIdx.x < tl.count) {
+                        const DMember& m = p.members[tl.member];
+                        int64_t i = tl.start + threadIdx.x;
+                        int64_t local = i / g.copies;
+                        exec_item(p, g, m, local, static_cast<int>(i - local * g.copies));
+                    }
+                }
+            }
+            if (g.flags & GF_BARRIER) grid_sync(grid);
+        }
+        // capture_probes (exec.cpp:328-338): shared probes read copy 0
+        if (p.n_probes) {
+            for (int q = 0; q < p.n_probes; ++q) {
+                const DProbe& pr = p.probes[q];
+                const int64_t n = static_cast<int64_t>(pr.dim) * B;
+                float* dst = p.ring + pr.ring_off + static_cast<int64_t>(ks) * pr.dim * B;
+                for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+                    int64_t d = i / B;
+                    int b = static_cast<int>(i - d * B);
+                    dst[i] = *at(p, pr.src, d, pr.per_batch ? b : 0);
+                }
+            }
+            grid_sync(grid);
+        }
+    }
+}
+
+// reset (exec.cpp:164-174): broadcast the pristine image to every copy
+__global__ void reset_kernel(float* arena, const float* pristine, const int64_t* base, const int64_t* pbase,
+                             const int64_t* span, const int32_t* per_batch, int nbuf, int B) {
+    for (int bi = blockIdx.y; bi < nbuf; bi += gridDim.y) {
+        const int copies = per_batch[bi] ? B : 1;
+        const int64_t n = span[bi] * copies;
+        for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+            int64_t e = i / copies;
+            arena[base[bi] + i] = pristine[pbase[bi] + e];
+        }
+    }
+}
+
+// [probe][n_steps][dim][B] -> [probe][B][n_steps][dim] (ProbeOutput's Tensor3 order)
+__global__ void probe_transpose_kernel(const float* ring, float* out, const int64_t* off, const int32_t* dims,
+                                       int nprobes, int steps, int B) {
+    for (int q = blockIdx.y; q < nprobes; q += gridDim.y) {
+        const int dim = dims[q];
+        const int64_t n = static_cast<int64_t>(steps) * dim * B;
+        for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+            // i indexes the output: ((b * steps) + s) * dim + d
+            int64_t d = i % dim;
+            int64_t s = (i / dim) % steps;
+            int64_t b = i / (static_cast<int64_t>(dim) * steps);
+            out[off[q] + i] = ring[off[q] + (s * dim + d) * B + b];
+        }
+    }
+}
+
+// Build the libm parity hash: insert (key, result) pairs, linear probing.
+__global__ void libm_hash_build_kernel(unsigned long long* slots, uint32_t mask, int shift, const uint32_t* keys,
+                                       const uint32_t* results, int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint32_t key = keys[i];
+        unsigned long long v = (static_cast<unsigned long long>(key) << 32) | results[i];
+        uint32_t s = (key * 0x9E3779B1u) >> shift;
+        for (;;) {
+            unsigned long long prev = atomicCAS(slots + s, 0ull, v);
+            if (prev == 0ull || prev == v) break;
+            s = (s + 1u) & mask;
+        }
+    }
+}
+
+// Device-side evaluation of the parity functions over a key range (tests).
+__global__ void libm_eval_kernel(int func, uint32_t lo, int64_t n, uint32_t* out, LibmTables t) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float x = __uint_as_float(static_cast<uint32_t>(lo + i));
+        float r = func == 0 ? glibc_expm1f(x, t) : glibc_log1pf(x, t);
+        out[i] = __float_as_uint(r);
+    }
+}
+
+// ---- host launchers --------------------------------------------------------
+
+cudaError_t launch_generic(const GenericProgram& p, int grid, int k_begin, int k_end, int call_k0,
+                           cudaStream_t stream) {
+    GenericProgram prog = p;
+    void* args[] = {&prog, &k_begin, &k_end, &call_k0};
+    if (grid <= 1) {
+        generic_run_kernel<<<1, kTile, 0, stream>>>(prog, k_begin, k_end, call_k0);
+        return cudaGetLastError();
+    }
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(generic_run_kernel), dim3(grid), dim3(kTile), args, 0,
+                                       stream);
+}
+
+int generic_max_coresident_blocks(int device) {
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, generic_run_kernel, kTile, 0);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    return per_sm * sms;
+}
+
+cudaError_t launch_reset(float* arena, const float* pristine, const int64_t* base, const int64_t* pbase,
+                         const int64_t* span, const int32_t* per_batch, int nbuf, int B, cudaStream_t stream) {
+    if (nbuf == 0) return cudaSuccess;
+    dim3 grid(64, nbuf < 1024 ? nbuf : 1024);
+    reset_kernel<<<grid, 256, 0, stream>>>(arena, pristine, base, pbase, span, per_batch, nbuf, B);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_probe_transpose(const float* ring, float* out, const int64_t* off, const int32_t* dims,
+                                   int nprobes, int steps, int B, cudaStream_t stream) {
+    if (nprobes == 0) return cudaSuccess;
+    dim3 grid(128, nprobes < 1024 ? nprobes : 1024);
+    probe_transpose_kernel<<<grid, 256, 0, stream>>>(ring, out, off, dims, nprobes, steps, B);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_libm_hash_build(unsigned long long* slots, uint32_t mask, int shift, const uint32_t* keys,
+                                   const uint32_t* results, int64_t n, cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    libm_hash_build_kernel<<<1184, 256, 0, stream>>>(slots, mask, shift, keys, results, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_libm_eval(int func, uint32_t lo, int64_t n, uint32_t* out, const LibmTables& t,
+                             cudaStream_t stream) {
+    libm_eval_kernel<<<1184, 256, 0, stream>>>(func, lo, n, out, t);
+    return cudaGetLastError();
+}
+
+}  // namespace nengb

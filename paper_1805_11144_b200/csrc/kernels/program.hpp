@@ -1,0 +1,98 @@
+// program.hpp — device program descriptors shared by the host compiler
+// (csrc/host/engine.cpp) and the CUDA kernels.  Plain PODs only.
+//
+// Device layout of every base buffer (BufferDesc, passes.hpp:63-70):
+//   shared    : float[span]                 element e at  base + e
+//   per-batch : float[span][B] (batch inner) element e, copy b at base + e*B + b
+// so an operand resolves to DArg{base, es, bs}: addr(e, b) = arena + base + e*es + b*bs
+// (es = B, bs = 1 per-batch; es = 1, bs = 0 shared).  This is the reference's
+// resolve() (exec.cpp:18-25) with its [b][span] copies transposed so a warp's
+// 32 lanes read 32 consecutive batch copies of one element.
+#pragma once
+
+#include <cstdint>
+
+namespace nengb {
+
+struct DArg {
+    int64_t base = 0;  // arena offset (floats) of element 0
+    int64_t elems = 0; // rows * elements-per-row of the operand
+    int32_t es = 1;    // element stride
+    int32_t bs = 0;    // batch stride
+};
+
+enum : int32_t {
+    GF_INC = 1,         // Copy: increment
+    GF_PER_BATCH = 2,   // run once per batch copy (exec.cpp:122-125)
+    GF_SERIAL_B = 4,    // per-batch group that writes shared storage: b copies in order
+    GF_SERIAL_ALL = 8,  // a member aliases itself with an offset: reference loop order, one thread
+    GF_HAS_STATE = 16,  // SimProcess with a state operand (tau > 0)
+    GF_BARRIER = 32,    // grid barrier after this group
+};
+
+enum : int32_t { MF_SCALAR_A = 1 };
+
+struct DMember {
+    DArg a[4];
+    int64_t value_at = 0;   // Reset payload offset
+    int64_t items = 0;      // work items per batch copy
+    float pes_scale = 0.f;  // (T)(rate*dt/n), SimPES (exec.cpp:291-292)
+    int32_t flags = 0;
+};
+
+struct DGroup {
+    int32_t kind = 0, flags = 0, neuron = 0;
+    int32_t member_begin = 0, n_members = 0;
+    int32_t tile_begin = 0, n_tiles = 0;
+    int32_t copies = 1;
+    float dt = 0.f, tau_a = 0.f, tau_b = 0.f, tau_rc = 0.f, tau_ref = 0.f, amplitude = 0.f;
+};
+
+// A tile is up to kTile consecutive work items of one member; item index
+// i = local * copies + b (batch innermost for coalescing).
+constexpr int kTile = 256;
+struct DTile {
+    int32_t member = 0, start = 0, count = 0;
+};
+
+struct DFeed {
+    DArg dst;
+    int32_t dim = 0, copies = 1;
+    int64_t data_off = 0;  // offset of this slot's [n_steps][dim][B] block in the call's feed buffer
+    int32_t present = 0;
+};
+
+struct DProbe {
+    DArg src;
+    int32_t dim = 0, per_batch = 0;
+    int64_t ring_off = 0;  // offset of this probe's [n_steps][dim][B] block in the call's ring
+};
+
+// glibc-parity tables for expm1f / log1pf (see csrc/tools/gen_libm_tables.c)
+struct LibmHash {
+    const unsigned long long* slots = nullptr;  // (key << 32) | result bits; 0 = empty
+    uint32_t mask = 0;
+    int32_t shift = 32;
+};
+struct LibmTables {
+    LibmHash t[3];  // 0: expm1f [-104,0)  1: log1pf [-1,0)  2: log1pf (0,inf)
+};
+
+struct GenericProgram {
+    float* arena = nullptr;
+    const DGroup* groups = nullptr;
+    const DMember* members = nullptr;
+    const DTile* tiles = nullptr;
+    const float* values = nullptr;
+    const DFeed* feeds = nullptr;
+    const DProbe* probes = nullptr;
+    int32_t n_groups = 0, n_feeds = 0, n_probes = 0, batch = 1;
+    int32_t any_feed = 0;
+    LibmTables libm;
+    // per call
+    const float* feed_data = nullptr;
+    float* ring = nullptr;
+    int32_t call_steps = 0;
+};
+
+}  // namespace nengb

@@ -1,0 +1,146 @@
+"""GpuEngine — Python face of the B200 executor (libneng_gpu.so, C ABI in
+include/neng_gpu.h).  Same surface as the reference's neng::EngineCore<float>
+(proj/include/nengine/exec.hpp:18-120): construct from a PlannedModel with a
+batch size and unroll factor, then run / reset / read_signal / buffer_storage /
+steps_completed.  There is no CPU path: if the native library is missing the
+import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+from . import _abi, ir
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libneng_gpu.so")
+
+MODE_AUTO, MODE_GENERIC, MODE_FUSED = 0, 1, 2
+
+_lib = None
+
+
+def lib():
+    """Load the native library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"native library missing: {LIB_PATH} — run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        L.neng_gpu_create.argtypes = [C.POINTER(_abi.neng_planned_model), C.c_int32, C.c_int32,
+                                      C.POINTER(_abi.neng_device_cfg), C.POINTER(P)]
+        L.neng_gpu_destroy.argtypes = [P]
+        L.neng_gpu_destroy.restype = None
+        L.neng_gpu_run.argtypes = [P, C.c_int32, C.c_int32, C.POINTER(_abi.neng_feed), C.POINTER(C.c_double)]
+        L.neng_gpu_run_device.argtypes = [P, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), P]
+        L.neng_gpu_synchronize.argtypes = [P]
+        L.neng_gpu_reset.argtypes = [P]
+        L.neng_gpu_read_signal.argtypes = [P, C.c_int32, C.c_int32, C.POINTER(C.c_double), C.c_int64,
+                                           C.POINTER(C.c_int64)]
+        L.neng_gpu_buffer_storage.argtypes = [P, C.c_int32, C.POINTER(C.c_int32)]
+        for fn in ("neng_gpu_batch", "neng_gpu_unroll", "neng_gpu_steps_completed", "neng_gpu_num_probes",
+                   "neng_gpu_mode"):
+            getattr(L, fn).argtypes = [P]
+            getattr(L, fn).restype = C.c_int32
+        L.neng_gpu_last_launch_count.argtypes = [P]
+        L.neng_gpu_last_launch_count.restype = C.c_int64
+        L.neng_gpu_last_error.argtypes = [P]
+        L.neng_gpu_last_error.restype = C.c_char_p
+        L.neng_last_error.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+class GpuEngine:
+    """Drop-in for EngineCore<float> on a B200.
+
+    ``mode``: MODE_AUTO picks the fused ensemble pipeline when the model is an
+    ensemble network it reproduces exactly, else the generic persistent
+    interpreter; MODE_GENERIC / MODE_FUSED force one (MODE_FUSED raises
+    BuildError if impossible).
+    """
+
+    def __init__(self, planned: ir.PlannedModel, batch: int = 1, unroll: int = 1, *, device: int = 0,
+                 mode: int = MODE_AUTO, steps_per_launch: int = 0):
+        L = lib()
+        self._planned = planned
+        self.model = planned.model
+        m = _abi.Marshalled()
+        view = _abi.planned_model_view(planned, m)
+        cfg = _abi.neng_device_cfg()
+        cfg.device, cfg.mode, cfg.steps_per_launch = device, mode, steps_per_launch
+        h = C.c_void_p()
+        st = L.neng_gpu_create(C.byref(view), batch, unroll, C.byref(cfg), C.byref(h))
+        if st:
+            _abi.raise_for(st, L.neng_last_error().decode())
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.neng_gpu_destroy(h)
+            self._h = None
+
+    def _check(self, st):
+        if st:
+            _abi.raise_for(st, lib().neng_gpu_last_error(self._h).decode())
+
+    # -- EngineCore surface --------------------------------------------------
+    def run(self, n_steps: int, feeds: Optional[ir.FeedData] = None) -> ir.ProbeOutput:
+        m = _abi.Marshalled()
+        nf, fv = _abi.feeds_view(feeds or {}, m)
+        total = _abi.probe_total(self.model, self.batch(), max(n_steps, 0))
+        out = np.zeros(max(total, 1))
+        self._check(lib().neng_gpu_run(self._h, n_steps, nf, fv, out.ctypes.data_as(_abi.f64p)))
+        return _abi.split_probes(self.model, out, self.batch(), n_steps)
+
+    def run_device(self, n_steps: int, feed_ptrs, probe_ptrs, stream: int = 0):
+        """Device-resident step loop: feed_ptrs / probe_ptrs are lists of raw
+        device pointers (ints or None), one per feed slot / probe."""
+        nfs = len(self.model.feed_slots)
+        fp = (C.c_void_p * max(nfs, 1))(*[C.c_void_p(p) if p else None for p in (feed_ptrs or [None] * nfs)])
+        npb = len(self.model.probes)
+        pp = (C.c_void_p * max(npb, 1))(*[C.c_void_p(p) if p else None for p in (probe_ptrs or [None] * npb)])
+        self._check(lib().neng_gpu_run_device(self._h, n_steps, fp, pp, C.c_void_p(stream) if stream else None))
+
+    def synchronize(self):
+        self._check(lib().neng_gpu_synchronize(self._h))
+
+    def reset(self):
+        self._check(lib().neng_gpu_reset(self._h))
+
+    def read_signal(self, sig: int, batch_index: int = 0) -> np.ndarray:
+        n = C.c_int64()
+        self._check(lib().neng_gpu_read_signal(self._h, sig, batch_index, None, 0, C.byref(n)))
+        out = np.zeros(max(n.value, 1))
+        self._check(lib().neng_gpu_read_signal(self._h, sig, batch_index, out.ctypes.data_as(_abi.f64p), n.value,
+                                               C.byref(n)))
+        return out[:n.value]
+
+    def buffer_storage(self, buffer: int) -> ir.StorageMode:
+        mode = C.c_int32()
+        self._check(lib().neng_gpu_buffer_storage(self._h, buffer, C.byref(mode)))
+        return ir.StorageMode(mode.value)
+
+    def batch(self) -> int:
+        return lib().neng_gpu_batch(self._h)
+
+    def unroll(self) -> int:
+        return lib().neng_gpu_unroll(self._h)
+
+    def steps_completed(self) -> int:
+        return lib().neng_gpu_steps_completed(self._h)
+
+    def planned(self) -> ir.PlannedModel:
+        return self._planned
+
+    # -- extras ---------------------------------------------------------------
+    def mode(self) -> int:
+        return lib().neng_gpu_mode(self._h)
+
+    def last_launch_count(self) -> int:
+        return lib().neng_gpu_last_launch_count(self._h)

@@ -1,0 +1,235 @@
+"""GPU parity: the B200 engine vs the reference's own EngineCore<float>
+(oracle/_ref, compiled from the reference sources) on the same PlannedModel.
+Cases mirror proj/tests/test_exec.cpp; the bar is bit-for-bit equality of
+every probe trace (the reference's tests use compare(...).max_abs_err == 0)."""
+import numpy as np
+import pytest
+
+from oracle import refapi
+from paper_1805_11144_b200 import ir
+from paper_1805_11144_b200.engine import MODE_GENERIC, GpuEngine
+from paper_1805_11144_b200.ir import Operator, SignalRef
+from tests.support.models import (assert_bitexact, batch_slice, chain_model, concat_steps, learning_model,
+                                  make_signal, pipeline_variants, step_slice, wave_feed)
+from tests.support.random_models import random_model
+
+pytestmark = pytest.mark.gpu
+
+
+def planify(model, cfg=None):
+    return refapi.run_passes(model, cfg).to_python()
+
+
+def ref_run(planned, batch, steps, feeds=None, unroll=1):
+    return refapi.RefEngine(planned, batch, unroll).run(steps, feeds)
+
+
+def test_constant_copy_reaches_probe_across_batch():
+    # test_exec.cpp:143-162
+    m = ir.BuiltModel()
+    m.signals = [make_signal(0, "c", [2], constant=True, initial=[0.5, -0.25]), make_signal(1, "t", [2])]
+    m.operators = [Operator.copy(0, SignalRef.full(m.signals[0]), SignalRef.full(m.signals[1]), False)]
+    m.probes = [ir.ProbeRegistration(0, 1, "t")]
+    pm = planify(m)
+    e = GpuEngine(pm, 3)
+    assert e.buffer_storage(pm.buffers.buffer_of[1]) == ir.StorageMode.Shared
+    out = e.run(4)
+    assert np.all(out[0][:, :, 0] == 0.5) and np.all(out[0][:, :, 1] == -0.25)
+    assert e.steps_completed() == 4
+    assert_bitexact(out, ref_run(pm, 3, 4))
+
+
+def test_shared_accumulator_advances_once_per_step():
+    # test_exec.cpp:164-177
+    m = ir.BuiltModel()
+    m.signals = [make_signal(0, "c", [1], constant=True, initial=[0.5]), make_signal(1, "acc", [1])]
+    m.operators = [Operator.copy(0, SignalRef.full(m.signals[0]), SignalRef.full(m.signals[1]), True)]
+    m.probes = [ir.ProbeRegistration(0, 1, "acc")]
+    pm = planify(m)
+    out = GpuEngine(pm, 4).run(6)
+    for s in range(6):
+        assert np.all(out[0][:, s, 0] == 0.5 * (s + 1))
+    assert_bitexact(out, ref_run(pm, 4, 6))
+
+
+def test_merged_copies_and_resets():
+    # test_exec.cpp:179-207
+    m = ir.BuiltModel()
+    m.signals = [make_signal(0, "c1", [2], initial=[0.1, 0.2]), make_signal(1, "c2", [2], initial=[0.3, 0.4]),
+                 make_signal(2, "t1", [2], minibatched=True), make_signal(3, "t2", [2], minibatched=True),
+                 make_signal(4, "r1", [2], minibatched=True), make_signal(5, "r2", [2], minibatched=True)]
+    f = lambda i: SignalRef.full(m.signals[i])  # noqa: E731
+    m.operators = [Operator.copy(0, f(0), f(2), False), Operator.copy(1, f(1), f(3), False),
+                   Operator.reset(2, f(4), [1.0, 2.0]), Operator.reset(3, f(5), [3.0, 4.0])]
+    m.probes = [ir.ProbeRegistration(s - 2, s, "p") for s in (2, 3, 4, 5)]
+    pm = planify(m)
+    assert len(pm.plan) == 2
+    out = GpuEngine(pm, 2).run(3)
+    assert out[0][1, 2, 0] == np.float64(np.float32(0.1))
+    assert out[3][0, 2, 1] == 4.0
+    assert_bitexact(out, ref_run(pm, 2, 3))
+
+
+@pytest.mark.parametrize("seed", range(1, 11))
+def test_random_models_bit_for_bit(seed):
+    # test_exec.cpp:209-224: 10 seeds x 5 pipeline variants x batch 1 and 4
+    model = random_model(seed, 45)
+    for vi, cfg in enumerate(pipeline_variants()):
+        pm = planify(model, cfg)
+        for batch in (1, 4):
+            gpu = GpuEngine(pm, batch).run(20)
+            assert_bitexact(gpu, ref_run(pm, batch, 20), f"seed {seed} variant {vi} batch {batch}")
+
+
+def test_built_networks_every_variant():
+    # test_exec.cpp:226-244
+    cm, node, _ = chain_model()
+    cfeeds = {node: wave_feed(1, 30, 2, 0.1)}
+    lm, nu, nt, _, _ = learning_model()
+    lfeeds = {nu: wave_feed(1, 30, 2, 0.2), nt: wave_feed(1, 30, 2, -0.3)}
+    for vi, cfg in enumerate(pipeline_variants()):
+        pc = planify(cm, cfg)
+        assert_bitexact(GpuEngine(pc).run(30, cfeeds), ref_run(pc, 1, 30, cfeeds), f"chain variant {vi}")
+        pl = planify(lm, cfg)
+        assert_bitexact(GpuEngine(pl).run(30, lfeeds), ref_run(pl, 1, 30, lfeeds), f"learning variant {vi}")
+
+
+def test_batch_equals_independent_runs():
+    # test_exec.cpp:246-267
+    lm, nu, nt, _, weights = learning_model()
+    B, S = 5, 25
+    feeds = {nu: wave_feed(B, S, 2, 0.2), nt: wave_feed(B, S, 2, -0.4)}
+    pm = planify(lm)
+    eb = GpuEngine(pm, B)
+    batched = eb.run(S, feeds)
+    assert_bitexact(batched, ref_run(pm, B, S, feeds))
+    for b in range(B):
+        single = GpuEngine(pm, 1)
+        solo = single.run(S, batch_slice(feeds, b))
+        for k in solo:
+            assert np.array_equal(batched[k][b], solo[k][0])
+        assert np.array_equal(single.read_signal(weights, 0), eb.read_signal(weights, b))
+
+
+def test_unroll_and_steps_per_launch_change_no_bits():
+    # test_exec.cpp:269-289 (+ the GPU's K-steps-per-launch knob)
+    rm = random_model(3, 40)
+    lm, nu, nt, _, _ = learning_model()
+    feeds = {nu: wave_feed(2, 23, 2, 0.2), nt: wave_feed(2, 23, 2, -0.4)}
+    pr, pl = planify(rm), planify(lm)
+    base_r = GpuEngine(pr, 2, 1).run(23)
+    base_l = GpuEngine(pl, 2, 1).run(23, feeds)
+    for unroll in (2, 5, 10):
+        assert_bitexact(GpuEngine(pr, 2, unroll).run(23), base_r)
+        el = GpuEngine(pl, 2, unroll, steps_per_launch=unroll)
+        assert_bitexact(el.run(23, feeds), base_l)
+        assert el.steps_completed() == 23 and el.unroll() == unroll
+
+
+def test_state_persists_across_calls():
+    # test_exec.cpp:291-310
+    cm, node, _ = chain_model()
+    feeds = {node: wave_feed(1, 30, 2, 0.15)}
+    pm = planify(cm)
+    full = GpuEngine(pm).run(30, feeds)
+    split = GpuEngine(pm)
+    head = split.run(12, step_slice(feeds, 0, 12))
+    tail = split.run(18, step_slice(feeds, 12, 18))
+    assert_bitexact(concat_steps(head, tail), full)
+    assert split.steps_completed() == 30
+    time_sig = next(s.id for s in pm.model.signals if s.label == "time")
+    assert split.read_signal(time_sig)[0] == np.float64(np.float32(30.0) * np.float32(0.001))
+
+
+def test_reset_restores_launch_state():
+    # test_exec.cpp:312-324
+    lm, nu, nt, _, _ = learning_model()
+    feeds = {nu: wave_feed(2, 20, 2, 0.2), nt: wave_feed(2, 20, 2, 0.5)}
+    e = GpuEngine(planify(lm), 2)
+    first = e.run(20, feeds)
+    assert e.steps_completed() == 20
+    e.reset()
+    assert e.steps_completed() == 0
+    assert_bitexact(e.run(20, feeds), first)
+
+
+def test_learned_weights_per_batch():
+    # test_exec.cpp:326-357
+    lm, nu, nt, _, weights = learning_model()
+    B = 3
+    inp = wave_feed(1, 40, 2, 0.2)
+    feeds = {nu: np.repeat(inp, B, axis=0), nt: wave_feed(B, 40, 2, -0.4)}
+    pm = planify(lm)
+    e = GpuEngine(pm, B)
+    assert e.buffer_storage(pm.buffers.buffer_of[weights]) == ir.StorageMode.PerBatch
+    e.run(40, feeds)
+    w = [e.read_signal(weights, b) for b in range(B)]
+    assert not np.array_equal(w[0], w[1]) and not np.array_equal(w[1], w[2])
+    ref = refapi.RefEngine(pm, B)
+    ref.run(40, feeds)
+    for b in range(B):
+        solo = GpuEngine(pm, 1)
+        solo.run(40, batch_slice(feeds, b))
+        assert np.array_equal(solo.read_signal(weights, 0), w[b])
+        assert np.array_equal(ref.read_signal(weights, b), w[b])
+
+
+def test_constant_weights_stay_shared():
+    # test_exec.cpp:359-371
+    cm, _, _ = chain_model()
+    conn_w = next(s.id for s in cm.signals if s.constant and s.trainable)
+    pm = planify(cm)
+    e = GpuEngine(pm, 3)
+    assert e.buffer_storage(pm.buffers.buffer_of[conn_w]) == ir.StorageMode.Shared
+    e.run(5)
+    assert np.array_equal(e.read_signal(conn_w, 0), e.read_signal(conn_w, 2))
+
+
+def test_feed_validation():
+    # test_exec.cpp:373-395 (messages identical to validate_feeds, model.hpp:62-83)
+    m = ir.BuiltModel()
+    m.signals = [make_signal(0, "node0.out", [2], minibatched=True), make_signal(1, "echo", [2], minibatched=True)]
+    m.operators = [Operator.copy(0, SignalRef.full(m.signals[0]), SignalRef.full(m.signals[1]), False)]
+    m.feed_slots = [ir.FeedSlot(0, 0, 2, False, "node0")]
+    m.probes = [ir.ProbeRegistration(0, 1, "echo")]
+    pm = planify(m)
+    e = GpuEngine(pm, 2)
+    with pytest.raises(ir.RunError, match="has no default output and no feed was supplied"):
+        e.run(5)
+    good = {0: wave_feed(2, 5, 2, 0.0)}
+    out = e.run(5, good)
+    assert out[0][1, 3, 0] == np.float64(np.float32(good[0][1, 3, 0]))
+    with pytest.raises(ir.RunError, match=r"expected \(2, >=5, 2\)"):
+        e.run(5, {0: wave_feed(2, 4, 2, 0.0)})
+    with pytest.raises(ir.RunError):
+        e.run(5, {0: wave_feed(3, 5, 2, 0.0)})
+    with pytest.raises(ir.RunError):
+        e.run(5, {0: wave_feed(2, 5, 1, 0.0)})
+    with pytest.raises(ir.RunError, match="feed for unknown node 99"):
+        e.run(5, {0: wave_feed(2, 5, 2, 0.0), 99: wave_feed(2, 5, 1, 0.0)})
+    with pytest.raises(ir.RunError, match="n_steps must be positive"):
+        e.run(0, good)
+
+
+def test_constructor_and_introspection_errors():
+    # test_exec.cpp:404-414
+    cm, _, _ = chain_model()
+    pm = planify(cm)
+    with pytest.raises(ir.BuildError, match="batch size"):
+        GpuEngine(pm, 0)
+    with pytest.raises(ir.BuildError, match="unroll"):
+        GpuEngine(pm, 1, 0)
+    e = GpuEngine(pm, 2)
+    for sig, b in ((-1, 0), (10000, 0), (0, 2), (0, -1)):
+        with pytest.raises(ir.RunError):
+            e.read_signal(sig, b)
+
+
+def test_generic_mode_is_forced_and_reported():
+    cm, node, _ = chain_model()
+    pm = planify(cm)
+    e = GpuEngine(pm, 1, mode=MODE_GENERIC)
+    assert e.mode() == MODE_GENERIC
+    feeds = {node: wave_feed(1, 10, 2, 0.1)}
+    assert_bitexact(e.run(10, feeds), ref_run(pm, 1, 10, feeds))
+    assert e.last_launch_count() >= 1
