@@ -91,6 +91,8 @@ class Engine {
     const std::vector<BufLayout>& layout() const { return bufs_; }
     float* arena() const { return arena_.as<float>(); }
     cudaStream_t stream() const { return stream_; }
+    int device() const { return device_; }
+    int steps_per_launch() const { return steps_per_launch_; }
 
   private:
     void compile();

@@ -1,11 +1,465 @@
-// fused_compile.cpp — placeholder until the fused ensemble pipeline lands.
+// fused_compile.cpp — recognise an ensemble network in a PlannedModel and
+// compile it to the fused two-phase pipeline (kernels/fused.cu).
+//
+// Recognised structure (the reference frontend's lowering, frontend.cpp:305-517,
+// in the unfolded form of SURVEY §8(d)):
+//   ensemble   Reset(in), Reset(J, bias), DotInc(E, in, J), SimNeurons(LIF, J, out, [v, r]),
+//              Reset(xhat), DotInc(D, out, xhat)
+//   connection Reset(acc), DotInc(T, src, acc), SimProcess(tau > 0, acc, filt, state),
+//              optionally Copy(filt -> in_dst, inc)          src = an ensemble's xhat or a fed node
+//   clock      TimeUpdate(step, time)
+// with no other accessor of any of these signals, every operand a full-signal
+// ref, every state per-batch and every weight a shared constant.  Anything
+// else returns nullptr and the engine keeps the generic interpreter.
+//
+// Why the two-phase schedule is the reference's arithmetic: every ordering
+// the plan imposes is a dependency edge (Set<Inc<Read<Update, ir.cpp:351-360)
+// except the order of increments into one target, and the only target with
+// several increments is `in`, whose Copy incs are summed in plan-group order
+// here.  The Copy reads `filt` before the SimProcess updates it (Read->Update
+// edge), so in(k) sums filt(k-1) == state(k-1); the connection DotInc reads
+// xhat(k) after its decoder increment and the fed value of step k.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <sstream>
+#include <unordered_map>
+
+#include "../kernels/fused.hpp"
+#include "engine.hpp"
 #include "fused.hpp"
 
 namespace nengb {
 
-std::unique_ptr<FusedPlan> try_compile_fused(Engine&, std::string* why) {
-    if (why) *why = "fused pipeline not built";
-    return nullptr;
+int fused_dmax_for(int d);
+cudaError_t launch_fused(const FusedProgram& p, int dmax, int grid, int k0, int k1, cudaStream_t stream);
+int fused_max_grid(const FusedProgram& p, int dmax, int device);
+
+namespace {
+
+struct Access {
+    int op;  // index into model.operators
+    int pos;
+    AccessMode mode;
+};
+
+struct Fail {
+    std::string why;
+};
+
+class FusedImpl : public FusedPlan {
+  public:
+    FusedProgram prog;
+    int dmax = 8, grid = 1, steps_per_launch = 0;
+    DevMem d_ens, d_conns, d_incoming, d_values, d_probes, d_feeds, d_call;
+    std::string desc;
+
+    int64_t run(int n_steps, const float* d_feed_data, const int64_t* feed_off, const int* present, float* d_ring,
+                const int64_t* ring_off, cudaStream_t stream) override {
+        // per-call tables: feed offsets, presence, ring offsets
+        const int nf = prog.n_feeds, np = n_probe_total;
+        std::vector<char> blob(static_cast<size_t>(nf) * 8 + static_cast<size_t>(np) * 8 + static_cast<size_t>(nf) * 4 + 64);
+        std::memcpy(blob.data(), feed_off, nf * 8);
+        std::memcpy(blob.data() + nf * 8, ring_off, np * 8);
+        std::memcpy(blob.data() + nf * 8 + np * 8, present, nf * 4);
+        d_call.ensure(blob.size());
+        cuda_check(cudaMemcpyAsync(d_call.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, stream), "fused call H2D");
+        FusedProgram p = prog;
+        p.feed_data = d_feed_data;
+        p.feed_off = d_call.as<int64_t>();
+        p.ring_off = reinterpret_cast<const int64_t*>(d_call.as<char>() + nf * 8);
+        p.feed_present = reinterpret_cast<const int32_t*>(d_call.as<char>() + nf * 8 + np * 8);
+        p.ring = d_ring;
+        p.call_steps = n_steps;
+        int K = steps_per_launch > 0 ? steps_per_launch : n_steps;
+        int64_t launches = 0;
+        for (int k = 0; k < n_steps; k += K) {
+            cuda_check(launch_fused(p, dmax, grid, k, std::min(n_steps, k + K), stream), "fused kernel launch");
+            ++launches;
+        }
+        cuda_check(cudaStreamSynchronize(stream), "fused run");  // call tables are reused next call
+        return launches;
+    }
+    void materialize(cudaStream_t) override {}
+    void load_from_arena(cudaStream_t) override {}
+    std::string describe() const override { return desc; }
+    int n_probe_total = 0;
+};
+
+bool is_full(const BuiltModel& m, const SignalRef& r) { return r.start == 0 && r.stop == m.signals[r.signal].rows(); }
+
+}  // namespace
+
+std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
+    const PlannedModel& pm = eng.planned();
+    const BuiltModel& m = pm.model;
+    const auto& L = eng.layout();
+    const int B = eng.batch();
+    try {
+        auto fail = [](const std::string& w) -> void { throw Fail{w}; };
+        const int nops = static_cast<int>(m.operators.size());
+        std::vector<std::vector<Access>> acc(m.signals.size());
+        for (int i = 0; i < nops; ++i) {
+            const Operator& op = m.operators[i];
+            for (auto [pos, mode] : operand_modes(op)) {
+                if (!is_full(m, op.operands[pos])) fail("operator " + std::to_string(op.id) + " uses a slice");
+                acc[op.operands[pos].signal].push_back({i, pos, mode});
+            }
+        }
+        std::unordered_map<int, int> group_of;  // op id -> plan group
+        for (size_t g = 0; g < pm.plan.size(); ++g)
+            for (int id : pm.plan[g].members) group_of[id] = static_cast<int>(g);
+        std::vector<char> claimed(nops, 0);
+        auto claim = [&](int i) {
+            if (claimed[i]) fail("operator " + std::to_string(m.operators[i].id) + " has two roles");
+            claimed[i] = 1;
+        };
+        auto per_batch = [&](int sig) { return L[pm.buffers.buffer_of[sig]].per_batch != 0; };
+        auto need_pb = [&](int sig, const char* what) {
+            if (!per_batch(sig)) fail(std::string(what) + " is not in per-batch storage");
+        };
+        auto need_shared_const = [&](int sig, const char* what) {
+            if (per_batch(sig) || !m.signals[sig].constant) fail(std::string(what) + " is not a shared constant");
+        };
+        auto op_at = [&](const Access& a) -> const Operator& { return m.operators[a.op]; };
+        // find the single Reset(Set) of a signal among its accessors
+        auto find_reset = [&](int sig) -> int {
+            int r = -1;
+            for (const Access& a : acc[sig])
+                if (op_at(a).kind == OpKind::Reset) {
+                    if (r >= 0) fail("signal '" + m.signals[sig].label + "' has two resets");
+                    r = a.op;
+                }
+            if (r < 0) fail("signal '" + m.signals[sig].label + "' has no reset");
+            return r;
+        };
+
+        std::vector<float> values;
+        auto push_values = [&](const std::vector<double>& v) {
+            int off = static_cast<int>(values.size());
+            for (double x : v) values.push_back(static_cast<float>(x));
+            return off;
+        };
+
+        struct EnsInfo {
+            int sn, enc, dec, rin, rj, rx;
+            int in, j, out, v, r, xhat, E, D;
+            std::vector<std::pair<int, int>> incs;  // (group, copy op index)
+        };
+        std::vector<EnsInfo> ens;
+        std::unordered_map<int, int> ens_of_in, ens_of_xhat;
+        for (int i = 0; i < nops; ++i) {
+            const Operator& op = m.operators[i];
+            if (op.kind != OpKind::SimNeurons) continue;
+            if (op.neuron.kind != NeuronKind::LIF) fail("non-LIF neurons");
+            EnsInfo e{};
+            e.sn = i;
+            e.j = op.operands[0].signal;
+            e.out = op.operands[1].signal;
+            e.v = op.operands[2].signal;
+            e.r = op.operands[3].signal;
+            for (int s : {e.j, e.out, e.v, e.r}) need_pb(s, "ensemble state");
+            for (int s : {e.v, e.r})
+                if (acc[s].size() != 1) fail("voltage/refractory has other accessors");
+            // J: Reset + DotInc(E, in, J) + this SimNeurons
+            if (acc[e.j].size() != 3) fail("J has extra accessors");
+            e.rj = find_reset(e.j);
+            e.enc = -1;
+            for (const Access& a : acc[e.j])
+                if (op_at(a).kind == OpKind::DotInc && a.pos == 2) e.enc = a.op;
+            if (e.enc < 0) fail("J has no encoder");
+            const Operator& enc = m.operators[e.enc];
+            e.E = enc.operands[0].signal;
+            e.in = enc.operands[1].signal;
+            need_shared_const(e.E, "encoders");
+            need_pb(e.in, "ensemble input");
+            // in: Reset + Copy incs + the encoder read
+            e.rin = find_reset(e.in);
+            for (const Access& a : acc[e.in]) {
+                const Operator& o = op_at(a);
+                if (a.op == e.rin || a.op == e.enc) continue;
+                if (o.kind == OpKind::Copy && o.inc && a.pos == 1)
+                    e.incs.push_back({group_of.at(o.id), a.op});
+                else
+                    fail("ensemble input has an unsupported accessor");
+            }
+            // out: this SimNeurons + one decoder DotInc
+            if (acc[e.out].size() != 2) fail("neuron output has extra readers");
+            e.dec = -1;
+            for (const Access& a : acc[e.out])
+                if (op_at(a).kind == OpKind::DotInc && a.pos == 1) e.dec = a.op;
+            if (e.dec < 0) fail("neuron output has no decoder");
+            const Operator& dec = m.operators[e.dec];
+            e.D = dec.operands[0].signal;
+            e.xhat = dec.operands[2].signal;
+            need_shared_const(e.D, "decoders");
+            need_pb(e.xhat, "decoded value");
+            e.rx = find_reset(e.xhat);
+            for (const Access& a : acc[e.xhat]) {
+                const Operator& o = op_at(a);
+                if (a.op == e.rx || a.op == e.dec) continue;
+                if (!(o.kind == OpKind::DotInc && a.pos == 1)) fail("decoded value has an unsupported accessor");
+            }
+            const Signal& Es = m.signals[e.E];
+            const Signal& Ds = m.signals[e.D];
+            int n = m.signals[e.j].rows(), d = m.signals[e.in].rows();
+            if (Es.shape.size() != 2 || Es.shape[0] != n || Es.shape[1] != d) fail("encoder shape");
+            if (Ds.shape.size() != 2 || Ds.shape[1] != n) fail("decoder shape");
+            if (!fused_dmax_for(std::max(d, Ds.shape[0]))) fail("dimension above 32");
+            for (double x : Ds.initial)
+                if (!std::isfinite(static_cast<float>(x))) fail("non-finite decoder weight");
+            for (int o : {e.sn, e.enc, e.dec, e.rin, e.rj, e.rx}) claim(o);
+            ens_of_in[e.in] = static_cast<int>(ens.size());
+            ens_of_xhat[e.xhat] = static_cast<int>(ens.size());
+            ens.push_back(std::move(e));
+        }
+        if (ens.empty()) fail("no LIF ensembles");
+
+        std::unordered_map<int, int> slot_of_sig;
+        for (size_t f = 0; f < m.feed_slots.size(); ++f) slot_of_sig[m.feed_slots[f].signal] = static_cast<int>(f);
+
+        struct ConnInfo {
+            int dot, rst, sp, copy;
+            int src, T, accs, filt, state;
+            int dst_ens;
+        };
+        std::vector<ConnInfo> conns;
+        std::unordered_map<int, int> conn_of_copy, conn_of_filt, conn_of_state;
+        for (int i = 0; i < nops; ++i) {
+            const Operator& op = m.operators[i];
+            if (op.kind != OpKind::DotInc || claimed[i]) continue;
+            ConnInfo c{};
+            c.dot = i;
+            c.T = op.operands[0].signal;
+            c.src = op.operands[1].signal;
+            c.accs = op.operands[2].signal;
+            need_shared_const(c.T, "transform");
+            need_pb(c.accs, "connection accumulator");
+            if (!ens_of_xhat.count(c.src)) {
+                if (!slot_of_sig.count(c.src)) fail("connection source is neither a decoded value nor a fed node");
+                need_pb(c.src, "fed node");
+                for (const Access& a : acc[c.src])
+                    if (!(op_at(a).kind == OpKind::DotInc && a.pos == 1)) fail("fed node has a writer or other reader");
+            }
+            if (acc[c.accs].size() != 3) fail("connection accumulator has extra accessors");
+            c.rst = find_reset(c.accs);
+            c.sp = -1;
+            for (const Access& a : acc[c.accs])
+                if (op_at(a).kind == OpKind::SimProcess && a.pos == 0) c.sp = a.op;
+            if (c.sp < 0) fail("connection without a lowpass synapse");
+            const Operator& sp = m.operators[c.sp];
+            if (!(sp.tau > 0.0) || sp.operands.size() != 3) fail("passthrough synapse (tau = 0)");
+            c.filt = sp.operands[1].signal;
+            c.state = sp.operands[2].signal;
+            need_pb(c.filt, "filtered value");
+            need_pb(c.state, "filter state");
+            if (acc[c.state].size() != 1) fail("filter state has other accessors");
+            {
+                const Signal& fs = m.signals[c.filt];
+                const Signal& ss = m.signals[c.state];
+                std::vector<double> fi = fs.initial, si = ss.initial;
+                if (fi.empty()) fi.assign(fs.size(), 0.0);
+                if (si.empty()) si.assign(ss.size(), 0.0);
+                if (fi != si) fail("filtered value and filter state start differently");
+            }
+            c.copy = -1;
+            c.dst_ens = -1;
+            for (const Access& a : acc[c.filt]) {
+                if (a.op == c.sp) continue;
+                const Operator& o = op_at(a);
+                if (o.kind == OpKind::Copy && a.pos == 0 && o.inc && ens_of_in.count(o.operands[1].signal) &&
+                    c.copy < 0) {
+                    c.copy = a.op;
+                    c.dst_ens = ens_of_in[o.operands[1].signal];
+                } else {
+                    fail("filtered value has an unsupported reader");
+                }
+            }
+            const Signal& Ts = m.signals[c.T];
+            int dd = m.signals[c.accs].rows(), ds = m.signals[c.src].rows();
+            if (Ts.shape.size() != 2 || Ts.shape[0] != dd || Ts.shape[1] != ds) fail("transform shape");
+            if (!fused_dmax_for(std::max(dd, ds))) fail("dimension above 32");
+            for (int o : {c.dot, c.rst, c.sp}) claim(o);
+            if (c.copy >= 0) {
+                claim(c.copy);
+                conn_of_copy[c.copy] = static_cast<int>(conns.size());
+            }
+            conn_of_filt[c.filt] = static_cast<int>(conns.size());
+            conn_of_state[c.state] = static_cast<int>(conns.size());
+            conns.push_back(c);
+        }
+        int time_op = -1;
+        for (int i = 0; i < nops; ++i) {
+            const Operator& op = m.operators[i];
+            if (op.kind == OpKind::TimeUpdate && !claimed[i]) {
+                if (time_op >= 0) fail("two clocks");
+                for (const SignalRef& r : op.operands) {
+                    if (acc[r.signal].size() != (op.operands[0].signal == op.operands[1].signal ? 2u : 1u))
+                        fail("clock signals have other accessors");
+                    if (per_batch(r.signal)) fail("per-batch clock");
+                }
+                time_op = i;
+                claim(i);
+            }
+        }
+        for (int i = 0; i < nops; ++i)
+            if (!claimed[i])
+                fail("operator " + std::to_string(m.operators[i].id) + " (" + op_kind_name(m.operators[i].kind) +
+                     ") is outside the ensemble pattern");
+        for (const EnsInfo& e : ens)
+            for (auto [g, ci] : e.incs)
+                if (!conn_of_copy.count(ci)) fail("ensemble input increment is not a connection");
+
+        // ---- descriptors -----------------------------------------------------
+        auto impl = std::make_unique<FusedImpl>();
+        FusedProgram& p = impl->prog;
+        const float dt = static_cast<float>(m.dt);
+        std::vector<FEns> fe;
+        std::vector<int32_t> incoming;
+        int nmax = 0, dmax_need = 1;
+        for (EnsInfo& e : ens) {
+            std::stable_sort(e.incs.begin(), e.incs.end());  // plan-group order of the Copy incs
+            for (size_t q = 1; q < e.incs.size(); ++q)
+                if (e.incs[q].first == e.incs[q - 1].first) fail("two increments of one input in one group");
+            FEns x{};
+            x.in_base = eng.resolve_full(e.in).base;
+            x.j_base = eng.resolve_full(e.j).base;
+            x.out_base = eng.resolve_full(e.out).base;
+            x.v_base = eng.resolve_full(e.v).base;
+            x.r_base = eng.resolve_full(e.r).base;
+            x.xhat_base = eng.resolve_full(e.xhat).base;
+            x.enc_base = eng.resolve_full(e.E).base;
+            x.dec_base = eng.resolve_full(e.D).base;
+            x.n = m.signals[e.j].rows();
+            x.d = m.signals[e.in].rows();
+            x.dx = m.signals[e.xhat].rows();
+            x.inc_begin = static_cast<int32_t>(incoming.size());
+            for (auto [g, ci] : e.incs) incoming.push_back(conn_of_copy.at(ci));
+            x.inc_count = static_cast<int32_t>(e.incs.size());
+            x.bias_off = push_values(m.operators[e.rj].value);
+            x.in_init_off = push_values(m.operators[e.rin].value);
+            x.xhat_init_off = push_values(m.operators[e.rx].value);
+            const NeuronModel& nm = m.operators[e.sn].neuron;
+            x.dt = dt;
+            x.tau_rc = static_cast<float>(nm.tau_rc);
+            x.tau_ref = static_cast<float>(nm.tau_ref);
+            x.amplitude = static_cast<float>(nm.amplitude);
+            volatile float num = x.amplitude, den = x.dt;  // float division, as amplitude / dt in T
+            x.amp_dt = num / den;
+            volatile float mdt = -x.dt, trc = x.tau_rc;
+            float arg = mdt / trc;
+            x.em_dt = expm1f(arg);  // the host libm result the reference uses
+            nmax = std::max(nmax, x.n);
+            dmax_need = std::max({dmax_need, x.d, x.dx});
+            fe.push_back(x);
+        }
+        std::vector<FConn> fc;
+        for (const ConnInfo& c : conns) {
+            FConn x{};
+            x.src_base = eng.resolve_full(c.src).base;
+            x.t_base = eng.resolve_full(c.T).base;
+            x.acc_base = eng.resolve_full(c.accs).base;
+            x.filt_base = eng.resolve_full(c.filt).base;
+            x.state_base = eng.resolve_full(c.state).base;
+            x.dd = m.signals[c.accs].rows();
+            x.ds = m.signals[c.src].rows();
+            x.acc_init_off = push_values(m.operators[c.rst].value);
+            const Operator& sp = m.operators[c.sp];
+            double a = std::exp(-m.dt / sp.tau);  // lowpass_coefficients (neuron_math.hpp:33-37)
+            x.a = static_cast<float>(a);
+            x.b = static_cast<float>(1.0 - a);
+            x.probe_filt = x.probe_state = -1;
+            dmax_need = std::max({dmax_need, x.dd, x.ds});
+            fc.push_back(x);
+        }
+        // probes
+        std::vector<FProbe> fp;
+        p.time_probe_step = p.time_probe_time = -1;
+        for (size_t q = 0; q < m.probes.size(); ++q) {
+            int s = m.probes[q].signal;
+            if (ens_of_xhat.count(s) || slot_of_sig.count(s)) {
+                FProbe pr{};
+                pr.base = eng.resolve_full(s).base;
+                pr.dim = static_cast<int32_t>(m.signals[s].size());
+                pr.per_batch = per_batch(s);
+                pr.index = static_cast<int32_t>(q);
+                fp.push_back(pr);
+            } else if (conn_of_filt.count(s)) {
+                FConn& x = fc[conn_of_filt[s]];
+                if (x.probe_filt >= 0) fail("two probes on one filtered value");
+                x.probe_filt = static_cast<int32_t>(q);
+            } else if (conn_of_state.count(s)) {
+                FConn& x = fc[conn_of_state[s]];
+                if (x.probe_state >= 0) fail("two probes on one filter state");
+                x.probe_state = static_cast<int32_t>(q);
+            } else if (time_op >= 0 && s == m.operators[time_op].operands[0].signal && p.time_probe_step < 0) {
+                p.time_probe_step = static_cast<int32_t>(q);
+            } else if (time_op >= 0 && s == m.operators[time_op].operands[1].signal && p.time_probe_time < 0) {
+                p.time_probe_time = static_cast<int32_t>(q);
+            } else {
+                fail("probe on '" + m.signals[s].label + "' (an on-chip intermediate)");
+            }
+        }
+        std::vector<FFeed> ff;
+        for (size_t f = 0; f < m.feed_slots.size(); ++f) {
+            FFeed x{};
+            x.base = eng.resolve_full(m.feed_slots[f].signal).base;
+            x.dim = m.feed_slots[f].dim;
+            x.copies = per_batch(m.feed_slots[f].signal) ? B : 1;
+            x.slot = static_cast<int32_t>(f);
+            ff.push_back(x);
+        }
+
+        auto upload = [](DevMem& d, const void* src, size_t bytes) {
+            d.ensure(std::max<size_t>(bytes, 16));
+            if (bytes) cuda_check(cudaMemcpy(d.p, src, bytes, cudaMemcpyHostToDevice), "fused H2D");
+        };
+        upload(impl->d_ens, fe.data(), fe.size() * sizeof(FEns));
+        upload(impl->d_conns, fc.data(), fc.size() * sizeof(FConn));
+        upload(impl->d_incoming, incoming.data(), incoming.size() * sizeof(int32_t));
+        upload(impl->d_values, values.data(), values.size() * sizeof(float));
+        upload(impl->d_probes, fp.data(), fp.size() * sizeof(FProbe));
+        upload(impl->d_feeds, ff.data(), ff.size() * sizeof(FFeed));
+        p.arena = eng.arena();
+        p.values = impl->d_values.as<float>();
+        p.ens = impl->d_ens.as<FEns>();
+        p.conns = impl->d_conns.as<FConn>();
+        p.incoming = impl->d_incoming.as<int32_t>();
+        p.probes = impl->d_probes.as<FProbe>();
+        p.feeds = impl->d_feeds.as<FFeed>();
+        p.n_ens = static_cast<int32_t>(fe.size());
+        p.n_conn = static_cast<int32_t>(fc.size());
+        p.n_probes = static_cast<int32_t>(fp.size());
+        p.n_feeds = static_cast<int32_t>(ff.size());
+        p.batch = B;
+        p.btiles = (B + 31) / 32;
+        p.nmax = (nmax + 31) / 32 * 32;
+        p.nwords = (nmax + 31) / 32;
+        p.dt = dt;
+        if (time_op >= 0) {
+            p.has_time = 1;
+            p.step_base = eng.resolve_full(m.operators[time_op].operands[0].signal).base;
+            p.time_base = eng.resolve_full(m.operators[time_op].operands[1].signal).base;
+        }
+        p.libm = libm_tables(eng.device());
+        impl->steps_per_launch = eng.steps_per_launch();
+        impl->n_probe_total = static_cast<int>(m.probes.size());
+        impl->dmax = fused_dmax_for(dmax_need);
+        int cap = fused_max_grid(p, impl->dmax, eng.device());
+        if (cap <= 0) fail("fused kernel does not fit on the device");
+        int64_t work = std::max<int64_t>(static_cast<int64_t>(p.n_ens) * p.btiles,
+                                         (static_cast<int64_t>(p.n_conn) * B + 255) / 256);
+        impl->grid = static_cast<int>(std::min<int64_t>(cap, std::max<int64_t>(1, work)));
+        std::ostringstream os;
+        os << "fused: " << p.n_ens << " ensembles, " << p.n_conn << " connections, dmax " << impl->dmax << ", grid "
+           << impl->grid;
+        impl->desc = os.str();
+        return impl;
+    } catch (const Fail& f) {
+        if (why) *why = f.why;
+        return nullptr;
+    }
 }
 
 }  // namespace nengb

@@ -1,0 +1,91 @@
+"""Fused ensemble pipeline parity: the fused kernel must leave every signal of
+every batch row bit-identical to the reference EngineCore<float> after every
+run() call (not only the probes), on the BASELINE workloads."""
+import numpy as np
+import pytest
+
+from oracle import refapi
+from paper_1805_11144_b200 import networks, passes
+from paper_1805_11144_b200.engine import MODE_FUSED, MODE_GENERIC, GpuEngine
+from tests.support.models import assert_bitexact, batch_slice, step_slice
+
+pytestmark = pytest.mark.gpu
+
+
+def full_state_equal(gpu, ref, model, batch, context):
+    for s in model.signals:
+        for b in {0, batch - 1}:
+            g, r = gpu.read_signal(s.id, b), ref.read_signal(s.id, b)
+            if not np.array_equal(g.view(np.uint64), r.view(np.uint64)):
+                i = int(np.argmax(g.view(np.uint64) != r.view(np.uint64)))
+                raise AssertionError(f"{context}: signal {s.label} row {b} elem {i}: {g[i]!r} vs {r[i]!r}")
+
+
+def small_network(seed=3, batch=4, steps=30):
+    return networks.random_network(seed, n_ens=8, n=64, d=4, k_out=3, n_inputs=3, batch=batch, steps=steps)
+
+
+def test_small_network_fused_bit_exact_full_state():
+    w = small_network()
+    pm = passes.run_passes(w.model)
+    gpu = GpuEngine(pm, w.batch)
+    assert gpu.mode() == MODE_FUSED
+    ref = refapi.RefEngine(pm, w.batch)
+    assert_bitexact(gpu.run(w.steps, w.feeds), ref.run(w.steps, w.feeds), "small fused")
+    full_state_equal(gpu, ref, pm.model, w.batch, "small fused")
+
+
+def test_fused_matches_generic_and_persists_across_calls():
+    w = small_network(seed=5, batch=33, steps=24)  # partial batch tile
+    pm = passes.run_passes(w.model)
+    fused, generic = GpuEngine(pm, w.batch), GpuEngine(pm, w.batch, mode=MODE_GENERIC)
+    assert fused.mode() == MODE_FUSED and generic.mode() == MODE_GENERIC
+    head = fused.run(10, step_slice(w.feeds, 0, 10))
+    tail = fused.run(14, step_slice(w.feeds, 10, 14))
+    whole = generic.run(24, w.feeds)
+    for k in whole:
+        assert np.array_equal(np.concatenate([head[k], tail[k]], axis=1).view(np.uint64), whole[k].view(np.uint64))
+    fused.reset()
+    assert_bitexact(fused.run(24, w.feeds), whole, "after reset")
+    k3 = GpuEngine(pm, w.batch, steps_per_launch=3)
+    assert_bitexact(k3.run(24, w.feeds), whole, "3 steps per launch")
+
+
+def test_config0_integrator_bit_exact():
+    w = networks.config0(steps=1000)
+    pm = passes.run_passes(w.model)
+    gpu = GpuEngine(pm, w.batch)
+    assert gpu.mode() == MODE_FUSED
+    ref = refapi.RefEngine(pm, w.batch)
+    assert_bitexact(gpu.run(w.steps, w.feeds), ref.run(w.steps, w.feeds), "config0")
+    full_state_equal(gpu, ref, pm.model, w.batch, "config0")
+
+
+def test_config2_shape_bit_exact():
+    # config 2 geometry (256 x 1024 LIF, d=16, K=4, 32 inputs); batch and steps reduced for the CPU reference
+    w = networks.random_network(1, 256, 1024, 16, 4, 32, batch=2, steps=12, name="config2_small")
+    pm = passes.run_passes(w.model)
+    gpu = GpuEngine(pm, w.batch)
+    assert gpu.mode() == MODE_FUSED
+    ref = refapi.RefEngine(pm, w.batch)
+    assert_bitexact(gpu.run(w.steps, w.feeds), ref.run(w.steps, w.feeds), "config2")
+    full_state_equal(gpu, ref, pm.model, w.batch, "config2")
+
+
+def test_config4_full_batch_sampled_rows_bit_exact():
+    # full config-4 geometry and batch (2048 x 512, d=8, K=8, 256 inputs, B=256) on the GPU;
+    # batch rows are independent (test_exec.cpp:246-267) so rows 0 and 255 are checked against
+    # solo reference engines fed the same row.
+    w = networks.config4(steps=6)
+    pm = passes.run_passes(w.model)
+    gpu = GpuEngine(pm, w.batch)
+    assert gpu.mode() == MODE_FUSED
+    out = gpu.run(w.steps, w.feeds)
+    for b in (0, w.batch - 1):
+        solo = refapi.RefEngine(pm, 1)
+        ref = solo.run(w.steps, batch_slice(w.feeds, b))
+        for k in ref:
+            assert np.array_equal(out[k][b:b + 1].view(np.uint64), ref[k].view(np.uint64)), f"row {b} probe {k}"
+        for s in pm.model.signals[::97]:
+            assert np.array_equal(gpu.read_signal(s.id, b).view(np.uint64), solo.read_signal(s.id, 0).view(np.uint64)), \
+                f"row {b} signal {s.label}"
