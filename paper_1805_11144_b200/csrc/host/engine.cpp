@@ -69,6 +69,9 @@ std::string library_dir() {
 
 struct HostTable {
     std::vector<uint32_t> keys, results;
+    double tmin = 0.0, tmin_hot = 0.0;
+    uint32_t region_shift = 0;
+    std::vector<float> regions;  // per-region minimum exception distance on [-1/16, 0)
 };
 
 std::vector<HostTable> load_libm_file() {
@@ -88,14 +91,25 @@ std::vector<HostTable> load_libm_file() {
     if (std::memcmp(magic, "NENGLIBM", 8)) throw BuildError("bad libm parity table file: " + path);
     uint32_t ver[2];
     take(ver, 8);
+    if (ver[0] != 4) throw BuildError("libm parity table file has version " + std::to_string(ver[0]) + ", want 4");
     std::vector<HostTable> out(3);
     for (uint32_t t = 0; t < ver[1]; ++t) {
-        uint32_t hdr[2];
+        uint32_t hdr[2], rh[2];
         uint64_t nkb;
+        double tmin, tmin_hot;
         take(hdr, 8);
+        take(&tmin, 8);
+        take(&tmin_hot, 8);
+        take(rh, 8);
+        std::vector<float> regions(rh[0]);
+        take(regions.data(), 4 * static_cast<size_t>(rh[0]));
         take(&nkb, 8);
         if (hdr[0] > 2) throw BuildError("bad libm table index");
         HostTable& ht = out[hdr[0]];
+        ht.tmin = tmin;
+        ht.tmin_hot = tmin_hot;
+        ht.region_shift = rh[1];
+        ht.regions = std::move(regions);
         size_t n = hdr[1];
         ht.keys.resize(n);
         ht.results.resize(n);
@@ -155,8 +169,9 @@ const LibmTables& libm_tables(int device) {
     if (it != g_libm.end()) return it->second->tables;
     std::vector<HostTable> host = load_libm_file();
     auto* dl = new DeviceLibm();
-    for (int t = 0; t < 3; ++t) {
-        size_t n = host[t].keys.size();
+    // open-addressing table at load factor <= 1/2 over (keys, results)
+    auto build = [&](const uint32_t* keys, const uint32_t* results, size_t n, const unsigned long long** slots_out,
+                     uint32_t* mask_out, int32_t* shift_out) {
         int log2cap = 4;
         while ((size_t{1} << log2cap) < 2 * n + 16) ++log2cap;
         size_t cap = size_t{1} << log2cap;
@@ -166,8 +181,8 @@ const LibmTables& libm_tables(int device) {
         void *dk = nullptr, *dr = nullptr;
         cuda_check(cudaMalloc(&dk, std::max<size_t>(n, 1) * 4), "cudaMalloc libm keys");
         cuda_check(cudaMalloc(&dr, std::max<size_t>(n, 1) * 4), "cudaMalloc libm results");
-        cuda_check(cudaMemcpy(dk, host[t].keys.data(), n * 4, cudaMemcpyHostToDevice), "libm H2D");
-        cuda_check(cudaMemcpy(dr, host[t].results.data(), n * 4, cudaMemcpyHostToDevice), "libm H2D");
+        cuda_check(cudaMemcpy(dk, keys, n * 4, cudaMemcpyHostToDevice), "libm H2D");
+        cuda_check(cudaMemcpy(dr, results, n * 4, cudaMemcpyHostToDevice), "libm H2D");
         cuda_check(launch_libm_hash_build(static_cast<unsigned long long*>(slots), static_cast<uint32_t>(cap - 1),
                                           32 - log2cap, static_cast<uint32_t*>(dk), static_cast<uint32_t*>(dr),
                                           static_cast<int64_t>(n), nullptr),
@@ -175,10 +190,35 @@ const LibmTables& libm_tables(int device) {
         cuda_check(cudaDeviceSynchronize(), "libm hash build");
         cudaFree(dk);
         cudaFree(dr);
-        dl->tables.t[t].slots = static_cast<const unsigned long long*>(slots);
-        dl->tables.t[t].mask = static_cast<uint32_t>(cap - 1);
-        dl->tables.t[t].shift = 32 - log2cap;
+        *slots_out = static_cast<const unsigned long long*>(slots);
+        *mask_out = static_cast<uint32_t>(cap - 1);
+        *shift_out = 32 - log2cap;
         dl->allocs.push_back(slots);
+    };
+    for (int t = 0; t < 3; ++t) {
+        const HostTable& ht = host[t];
+        build(ht.keys.data(), ht.results.data(), ht.keys.size(), &dl->tables.t[t].slots, &dl->tables.t[t].mask,
+              &dl->tables.t[t].shift);
+        // the LIF range x in [-1/16, 0) (bit patterns 0x80000001..0xBD800000) as a small, L2-resident table
+        auto lo = std::lower_bound(ht.keys.begin(), ht.keys.end(), 0x80000001u);
+        auto hi = std::upper_bound(ht.keys.begin(), ht.keys.end(), 0xBD800000u);
+        size_t a = static_cast<size_t>(lo - ht.keys.begin()), b = static_cast<size_t>(hi - ht.keys.begin());
+        build(ht.keys.data() + a, ht.results.data() + a, b > a ? b - a : 0, &dl->tables.t[t].hot_slots,
+              &dl->tables.t[t].hot_mask, &dl->tables.t[t].hot_shift);
+        // skip lookups whose double result is farther than this from a float
+        // rounding midpoint (all exceptions are closer); margin covers the
+        // device/host double results differing by a few double ulps
+        dl->tables.t[t].lookup_from = static_cast<float>(host[t].tmin - 0.01);
+        dl->tables.t[t].lookup_from_hot = static_cast<float>(host[t].tmin_hot - 0.01);
+        std::vector<float> reg(ht.regions.size());
+        for (size_t i = 0; i < reg.size(); ++i) reg[i] = ht.regions[i] - 0.01f;  // same margin
+        void* dreg = nullptr;
+        cuda_check(cudaMalloc(&dreg, std::max<size_t>(reg.size(), 1) * 4), "cudaMalloc libm regions");
+        cuda_check(cudaMemcpy(dreg, reg.data(), reg.size() * 4, cudaMemcpyHostToDevice), "libm regions H2D");
+        dl->allocs.push_back(dreg);
+        dl->tables.t[t].region_from = static_cast<const float*>(dreg);
+        dl->tables.t[t].region_shift = ht.region_shift;
+        dl->tables.t[t].n_regions = static_cast<uint32_t>(reg.size());
     }
     g_libm[device] = dl;
     return dl->tables;

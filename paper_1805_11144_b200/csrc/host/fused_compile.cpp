@@ -20,6 +20,8 @@
 // edge), so in(k) sums filt(k-1) == state(k-1); the connection DotInc reads
 // xhat(k) after its decoder increment and the fed value of step k.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -52,7 +54,7 @@ class FusedImpl : public FusedPlan {
   public:
     FusedProgram prog;
     int dmax = 8, grid = 1, steps_per_launch = 0;
-    DevMem d_ens, d_conns, d_incoming, d_values, d_probes, d_feeds, d_call;
+    DevMem d_ens, d_conns, d_incoming, d_values, d_probes, d_feeds, d_call, d_prof, d_work;
     std::string desc;
 
     int64_t run(int n_steps, const float* d_feed_data, const int64_t* feed_off, const int* present, float* d_ring,
@@ -72,13 +74,34 @@ class FusedImpl : public FusedPlan {
         p.feed_present = reinterpret_cast<const int32_t*>(d_call.as<char>() + nf * 8 + np * 8);
         p.ring = d_ring;
         p.call_steps = n_steps;
+        const bool profile = std::getenv("NENG_FUSED_PROFILE") != nullptr;
+        if (profile) {
+            d_prof.ensure(FS_COUNT * 8);
+            cuda_check(cudaMemsetAsync(d_prof.p, 0, FS_COUNT * 8, stream), "profile reset");
+            p.prof = d_prof.as<unsigned long long>();
+        }
+        d_work.ensure(16);
+        p.work = d_work.as<int32_t>();
         int K = steps_per_launch > 0 ? steps_per_launch : n_steps;
         int64_t launches = 0;
         for (int k = 0; k < n_steps; k += K) {
+            cuda_check(cudaMemsetAsync(d_work.p, 0, 8, stream), "fused work reset");
             cuda_check(launch_fused(p, dmax, grid, k, std::min(n_steps, k + K), stream), "fused kernel launch");
             ++launches;
         }
         cuda_check(cudaStreamSynchronize(stream), "fused run");  // call tables are reused next call
+        if (profile) {
+            unsigned long long h[FS_COUNT];
+            cuda_check(cudaMemcpy(h, d_prof.p, sizeof h, cudaMemcpyDeviceToHost), "profile D2H");
+            static const char* names[FS_COUNT] = {"feed",      "A1 in+stage", "A2 lif", "A2 fixup", "A3 transpose",
+                                                  "A4 decode", "barrier1",    "B conn", "barrier2"};
+            double tot = 0;
+            for (unsigned long long x : h) tot += static_cast<double>(x);
+            std::fprintf(stderr, "[fused profile] %d steps, grid %d: per-step per-CTA us:", n_steps, grid);
+            for (int s = 0; s < FS_COUNT; ++s)
+                std::fprintf(stderr, " %s=%.1f", names[s], h[s] / 1e3 / grid / n_steps);
+            std::fprintf(stderr, " (total %.1f)\n", tot / 1e3 / grid / n_steps);
+        }
         return launches;
     }
     void materialize(cudaStream_t) override {}
@@ -316,8 +339,17 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         FusedProgram& p = impl->prog;
         const float dt = static_cast<float>(m.dt);
         std::vector<FEns> fe;
-        std::vector<int32_t> incoming;
-        int nmax = 0, dmax_need = 1;
+        std::vector<int64_t> incoming;
+        int nmax = 0, dmax_need = 1, pmax_floats = 0;
+        for (const EnsInfo& e : ens)
+            dmax_need = std::max({dmax_need, m.signals[e.in].rows(), m.signals[e.xhat].rows()});
+        for (const ConnInfo& c : conns)
+            dmax_need = std::max({dmax_need, m.signals[c.accs].rows(), m.signals[c.src].rows()});
+        const int DMAX = fused_dmax_for(dmax_need);
+        auto align4 = [&] {
+            while (values.size() % 4) values.push_back(0.0f);
+            return static_cast<int64_t>(values.size());
+        };
         for (EnsInfo& e : ens) {
             std::stable_sort(e.incs.begin(), e.incs.end());  // plan-group order of the Copy incs
             for (size_t q = 1; q < e.incs.size(); ++q)
@@ -335,9 +367,22 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             x.d = m.signals[e.in].rows();
             x.dx = m.signals[e.xhat].rows();
             x.inc_begin = static_cast<int32_t>(incoming.size());
-            for (auto [g, ci] : e.incs) incoming.push_back(conn_of_copy.at(ci));
+            for (auto [g, ci] : e.incs) incoming.push_back(eng.resolve_full(conns[conn_of_copy.at(ci)].state).base);
             x.inc_count = static_cast<int32_t>(e.incs.size());
-            x.bias_off = push_values(m.operators[e.rj].value);
+            x.n_pad = (x.n + 3) / 4 * 4;
+            x.bias_off = align4();
+            push_values(m.operators[e.rj].value);
+            while (static_cast<int64_t>(values.size()) < x.bias_off + x.n_pad) values.push_back(0.0f);
+            {
+                // encoder rows zero padded to DMAX (exact: see fused.cu)
+                const Signal& Es = m.signals[e.E];
+                x.epad_off = align4();
+                for (int ii = 0; ii < x.n; ++ii)
+                    for (int jj = 0; jj < DMAX; ++jj)
+                        values.push_back(jj < x.d && !Es.initial.empty()
+                                             ? static_cast<float>(Es.initial[static_cast<size_t>(ii) * x.d + jj])
+                                             : 0.0f);
+            }
             x.in_init_off = push_values(m.operators[e.rin].value);
             x.xhat_init_off = push_values(m.operators[e.rx].value);
             const NeuronModel& nm = m.operators[e.sn].neuron;
@@ -350,6 +395,19 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             volatile float mdt = -x.dt, trc = x.tau_rc;
             float arg = mdt / trc;
             x.em_dt = expm1f(arg);  // the host libm result the reference uses
+            {
+                // spike products fp32(D[r,i]) * amp_dt: the DotInc term for out[i] = amp/dt
+                const Signal& Ds = m.signals[e.D];
+                x.dec_scaled_off = align4();
+                x.dec_bytes = (x.n * x.dx * 4 + 15) / 16 * 16;
+                pmax_floats = std::max(pmax_floats, x.dec_bytes / 4);
+                for (int ii = 0; ii < x.n; ++ii)  // transposed: [n][dx]
+                    for (int rr = 0; rr < x.dx; ++rr) {
+                        double dv = Ds.initial.empty() ? 0.0 : Ds.initial[static_cast<size_t>(rr) * x.n + ii];
+                        volatile float w = static_cast<float>(dv);
+                        values.push_back(w * x.amp_dt);
+                    }
+            }
             nmax = std::max(nmax, x.n);
             dmax_need = std::max({dmax_need, x.d, x.dx});
             fe.push_back(x);
@@ -364,7 +422,21 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             x.state_base = eng.resolve_full(c.state).base;
             x.dd = m.signals[c.accs].rows();
             x.ds = m.signals[c.src].rows();
+            x.src_feed = -1;
+            if (slot_of_sig.count(c.src)) {
+                x.src_feed = slot_of_sig[c.src];
+                if (m.feed_slots[x.src_feed].dim != x.ds) fail("feed slot dim differs from its signal");
+            }
             x.acc_init_off = push_values(m.operators[c.rst].value);
+            {
+                const Signal& Ts = m.signals[c.T];
+                x.tpad_off = align4();
+                for (int rr = 0; rr < x.dd; ++rr)
+                    for (int jj = 0; jj < DMAX; ++jj)
+                        values.push_back(jj < x.ds && !Ts.initial.empty()
+                                             ? static_cast<float>(Ts.initial[static_cast<size_t>(rr) * x.ds + jj])
+                                             : 0.0f);
+            }
             const Operator& sp = m.operators[c.sp];
             double a = std::exp(-m.dt / sp.tau);  // lowpass_coefficients (neuron_math.hpp:33-37)
             x.a = static_cast<float>(a);
@@ -384,6 +456,9 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
                 pr.dim = static_cast<int32_t>(m.signals[s].size());
                 pr.per_batch = per_batch(s);
                 pr.index = static_cast<int32_t>(q);
+                pr.feed_slot = slot_of_sig.count(s) ? slot_of_sig[s] : -1;
+                if (pr.feed_slot >= 0 && m.feed_slots[pr.feed_slot].dim != pr.dim)
+                    fail("feed slot dim differs from its signal");
                 fp.push_back(pr);
             } else if (conn_of_filt.count(s)) {
                 FConn& x = fc[conn_of_filt[s]];
@@ -417,7 +492,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         };
         upload(impl->d_ens, fe.data(), fe.size() * sizeof(FEns));
         upload(impl->d_conns, fc.data(), fc.size() * sizeof(FConn));
-        upload(impl->d_incoming, incoming.data(), incoming.size() * sizeof(int32_t));
+        upload(impl->d_incoming, incoming.data(), incoming.size() * sizeof(int64_t));
         upload(impl->d_values, values.data(), values.size() * sizeof(float));
         upload(impl->d_probes, fp.data(), fp.size() * sizeof(FProbe));
         upload(impl->d_feeds, ff.data(), ff.size() * sizeof(FFeed));
@@ -425,7 +500,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         p.values = impl->d_values.as<float>();
         p.ens = impl->d_ens.as<FEns>();
         p.conns = impl->d_conns.as<FConn>();
-        p.incoming = impl->d_incoming.as<int32_t>();
+        p.incoming = impl->d_incoming.as<int64_t>();
         p.probes = impl->d_probes.as<FProbe>();
         p.feeds = impl->d_feeds.as<FFeed>();
         p.n_ens = static_cast<int32_t>(fe.size());
@@ -436,6 +511,14 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         p.btiles = (B + 31) / 32;
         p.nmax = (nmax + 31) / 32 * 32;
         p.nwords = (nmax + 31) / 32;
+        p.pmax_floats = pmax_floats;
+        // stage the decoder products with the encoders when the CTA's shared
+        // memory stays small enough for three CTAs per SM
+        {
+            size_t base = 128 + static_cast<size_t>(p.nmax) * DMAX * 4 + static_cast<size_t>(p.nmax) * 8 +
+                          DMAX * 128 + static_cast<size_t>(p.nwords) * 128 + 1024 * 16;
+            p.stage_dec = base + static_cast<size_t>(pmax_floats) * 4 <= 72 * 1024 ? 1 : 0;
+        }
         p.dt = dt;
         if (time_op >= 0) {
             p.has_time = 1;

@@ -73,6 +73,16 @@ struct LibmHash {
     const unsigned long long* slots = nullptr;  // (key << 32) | result bits; 0 = empty
     uint32_t mask = 0;
     int32_t shift = 32;
+    float lookup_from = 0.f;      // probe only when the result is >= this many ulps from the rounded float
+    float lookup_from_hot = 0.f;  // the same bound restricted to x in [-1/16, 0) (the LIF range)
+    // the x in [-1/16, 0) subset as its own small (L2-resident) table
+    const unsigned long long* hot_slots = nullptr;
+    uint32_t hot_mask = 0;
+    int32_t hot_shift = 32;
+    // per-region bounds on [-1/16, 0): region = (key - 0x80000000) >> region_shift
+    const float* region_from = nullptr;
+    uint32_t region_shift = 31;
+    uint32_t n_regions = 0;
 };
 struct LibmTables {
     LibmHash t[3];  // 0: expm1f [-104,0)  1: log1pf [-1,0)  2: log1pf (0,inf)

@@ -17,8 +17,10 @@
  * device's double-then-round was found to differ from the host's).
  *
  * File format (little endian):
- *   "NENGLIBM" u32 version=1 u32 n_tables
- *   per table: u32 func, u32 count, u64 n_key_bytes, varint key deltas,
+ *   "NENGLIBM" u32 version=4 u32 n_tables
+ *   per table: u32 index, u32 count, f64 tmin, f64 tmin on [-1/16,0),
+ *              u32 n_regions, u32 region_shift, f32 region tmin[n_regions],
+ *              u64 n_key_bytes, varint key deltas,
  *              2-bit codes (0: host_dtr-1ulp, 1: host_dtr+1ulp, 2: host_dtr), 4 per byte
  * Usage: gen_libm_tables OUT [THREADS] [OVERRIDES]
  */
@@ -169,7 +171,52 @@ static void add_overrides(Table* tb, int func, const char* path) {
     tb->n = o;
 }
 
-static void write_table(FILE* out, int func, const Table* tb) {
+/* Distance (in float ulps) of the double result from the float it rounds
+ * to, for the smallest such distance among a table's exceptions.  glibc's
+ * float routines are ~0.53 ulp accurate, so every exception lies near a
+ * rounding midpoint (t close to 0.5); the device skips the table lookup when
+ * its own t is below this minimum (minus a margin). */
+static double exception_tmin(int func, const Table* tb, int hot_only) {
+    double tmin = 0.5;
+    for (size_t i = 0; i < tb->n; ++i) {
+        float x = f_of(tb->keys[i]);
+        if (hot_only && !(x >= -0.0625f && x < 0.0f)) continue;
+        double y = func == 0 ? expm1((double)x) : log1p((double)x);
+        float r = (float)y;
+        float up = nextafterf(r, INFINITY), dn = nextafterf(r, -INFINITY);
+        double ulp = (double)up - (double)r;
+        if (y < (double)r) ulp = (double)r - (double)dn;
+        if (!(ulp > 0)) continue;
+        double t = fabs(y - (double)r) / ulp;
+        if (t < tmin) tmin = t;
+    }
+    return tmin;
+}
+
+/* Per-region minimum exception distance over the LIF range x in [-1/16, 0)
+ * (bit patterns 0x80000001..0xBD800000, region = (key - 0x80000000) >> 18):
+ * 1.0 for regions without exceptions.  Lets the device skip ~2/3 of the
+ * probes the single hot-range bound would take. */
+#define REGION_SHIFT 18
+#define REGIONS (((0xBD800000u - 0x80000000u) >> REGION_SHIFT) + 1)
+static void region_tmin(int func, const Table* tb, float* out) {
+    for (unsigned i = 0; i < REGIONS; ++i) out[i] = 1.0f;
+    for (size_t i = 0; i < tb->n; ++i) {
+        uint32_t k = tb->keys[i];
+        if (k < 0x80000001u || k > 0xBD800000u) continue;
+        float x = f_of(k);
+        double y = func == 0 ? expm1((double)x) : log1p((double)x);
+        float r = (float)y;
+        float up = nextafterf(r, INFINITY), dn = nextafterf(r, -INFINITY);
+        double ulp = y < (double)r ? (double)r - (double)dn : (double)up - (double)r;
+        if (!(ulp > 0)) continue;
+        double t = fabs(y - (double)r) / ulp;
+        unsigned reg = (k - 0x80000000u) >> REGION_SHIFT;
+        if (t < out[reg]) out[reg] = (float)t;
+    }
+}
+
+static void write_table(FILE* out, int func, const Table* tb, double tmin, double tmin_hot) {
     uint8_t* kb = malloc(tb->n * 5 + 16);
     size_t nk = 0;
     uint32_t prev = 0;
@@ -185,6 +232,15 @@ static void write_table(FILE* out, int func, const Table* tb) {
     uint32_t hdr[2] = {(uint32_t)func, (uint32_t)tb->n};
     uint64_t nkb = nk;
     fwrite(hdr, 4, 2, out);
+    fwrite(&tmin, 8, 1, out);
+    fwrite(&tmin_hot, 8, 1, out);
+    {
+        static float reg[REGIONS];
+        uint32_t rh[2] = {REGIONS, REGION_SHIFT};
+        region_tmin(func == 0 ? 0 : 1, tb, reg);
+        fwrite(rh, 4, 2, out);
+        fwrite(reg, 4, REGIONS, out);
+    }
     fwrite(&nkb, 8, 1, out);
     fwrite(kb, 1, nk, out);
     size_t ncb = (tb->n + 3) / 4;
@@ -219,14 +275,17 @@ int main(int argc, char** argv) {
         return 1;
     }
     fwrite("NENGLIBM", 1, 8, out);
-    uint32_t ver[2] = {1, 3};
+    uint32_t ver[2] = {4, 3};
     fwrite(ver, 4, 2, out);
     for (int t = 0; t < 3; ++t) {
         Table tb = run_table(spec[t].func, spec[t].lo, spec[t].hi, threads);
         /* overrides are keyed by table index */
         add_overrides(&tb, t, overrides);
-        write_table(out, t, &tb);
-        fprintf(stderr, "table %d: %zu entries\n", t, tb.n);
+        double tmin = exception_tmin(spec[t].func, &tb, 0);
+        double tmin_hot = exception_tmin(spec[t].func, &tb, 1);
+        write_table(out, t, &tb, tmin, tmin_hot);
+        fprintf(stderr, "table %d: %zu entries, min exception distance %.4f ulp (%.4f on [-1/16, 0))\n", t, tb.n,
+                tmin, tmin_hot);
         free(tb.keys);
         free(tb.codes);
     }

@@ -191,6 +191,38 @@ class NetBuilder:
         return key
 
 
+def algorithmic_bytes_per_step(model: ir.BuiltModel, batch: int) -> int:
+    """HBM bytes one timestep must move at minimum:
+    4 * [ 4*N*B          LIF v, r read + write
+        + N              J bias payload
+        + sum n*d        encoders       + sum d*n  decoders
+        + sum dd*ds      transforms     + 2*sum dd*B  lowpass state read + write
+        + sum dim*B      feeds          + sum dim*B   probes ]
+    Transients (J, out, in, xhat, acc) are excluded: a fused kernel keeps them
+    on-chip.  Counted from the model's operators, so it holds for any
+    ensemble network built by NetBuilder."""
+    s = model.signals
+    floats = 0
+    for op in model.operators:
+        k = op.kind
+        if k == ir.OpKind.SimNeurons and op.neuron.kind == ir.NeuronKind.LIF:
+            floats += 4 * s[op.operands[0].signal].size() * batch
+        elif k == ir.OpKind.Reset and s[op.operands[0].signal].label.endswith(".J"):
+            floats += s[op.operands[0].signal].size()
+        elif k == ir.OpKind.DotInc:
+            floats += s[op.operands[0].signal].size()
+        elif k == ir.OpKind.SimProcess and op.tau > 0:
+            floats += 2 * s[op.operands[0].signal].size() * batch
+    floats += sum(f.dim for f in model.feed_slots) * batch
+    floats += sum(s[p.signal].size() for p in model.probes) * batch
+    return 4 * floats
+
+
+def neuron_count(model: ir.BuiltModel) -> int:
+    return sum(model.signals[op.operands[0].signal].size() for op in model.operators
+               if op.kind == ir.OpKind.SimNeurons)
+
+
 # ---------------------------------------------------------------------------
 # BASELINE.json configurations
 
