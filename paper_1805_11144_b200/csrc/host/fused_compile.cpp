@@ -516,7 +516,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         // memory stays small enough for three CTAs per SM
         {
             size_t base = 128 + static_cast<size_t>(p.nmax) * DMAX * 4 + static_cast<size_t>(p.nmax) * 8 +
-                          DMAX * 128 + static_cast<size_t>(p.nwords) * 128 + 1024 * 16;
+                          DMAX * 128 + static_cast<size_t>(p.nwords) * 128 + 1024 * 16 + 8 * 13 * 32 * 4;
             p.stage_dec = base + static_cast<size_t>(pmax_floats) * 4 <= 72 * 1024 ? 1 : 0;
         }
         p.dt = dt;

@@ -307,7 +307,7 @@ __device__ void phase_a_unit(const FusedProgram& p, int unit, bool last, const S
                 }
             }
             const uint32_t word = __ballot_sync(0xffffffffu, spike_final);
-            if (live) {
+            if (valid) {
                 __stcs(vcol + i * B, vo);
                 __stcs(rcol + i * B, ro);
                 if (last) {
@@ -323,16 +323,53 @@ __device__ void phase_a_unit(const FusedProgram& p, int unit, bool last, const S
 
     // A2': exact resolution of the queued neurons (all threads, probes overlap)
     const int nfix = min(*S.nfix, kFixCap);
+    // Stage 1 re-derives the speculative arguments and probes the tables for
+    // both at once; only a real glibc exception (~0.6% of queued neurons)
+    // triggers the exact recomputation and the patch.
     for (int f = threadIdx.x; f < nfix; f += kThreads) {
         const FixEntry fe = S.fix[f];
         const int i = fe.key >> 5, l = fe.key & 31;
+        float delta = dt - fe.r;
+        if (delta < 0.0f) delta = 0.0f;
+        if (delta > dt) delta = dt;
+        const float xe = -delta / tau_rc;
+        const bool pe = delta != dt && delta != 0.0f && lif_range(xe);
+        float em = delta == dt ? em_dt : -0.0f;
+        bool de = false;
+        if (delta != dt && delta != 0.0f) {
+            if (pe) {
+                const Spec s = spec_lif(xe, false, p.libm);
+                em = s.r;
+                de = s.doubtful;
+            } else {
+                em = glibc_expm1f(xe, p.libm);
+            }
+        }
+        float vn = fe.v - (fe.J - fe.v) * em;
+        if (vn < 0.0f) vn = 0.0f;
+        const float xl = -(vn - 1.0f) / (fe.J - 1.0f);
+        const bool dl = vn > 1.0f && lif_range(xl) && spec_lif(xl, true, p.libm).doubtful;
+        const LibmHash &h0 = p.libm.t[0], &h1 = p.libm.t[1];
+        const uint32_t ke = __float_as_uint(xe), kl = __float_as_uint(xl);
+        uint32_t ie = (ke * 0x9E3779B1u) >> h0.hot_shift, il = (kl * 0x9E3779B1u) >> h1.hot_shift;
+        unsigned long long se = de ? __ldg(h0.hot_slots + ie) : 0ull;  // both first probes in flight
+        unsigned long long sl = dl ? __ldg(h1.hot_slots + il) : 0ull;
+        while (se != 0ull && static_cast<uint32_t>(se >> 32) != ke) {
+            ie = (ie + 1u) & h0.hot_mask;
+            se = __ldg(h0.hot_slots + ie);
+        }
+        while (sl != 0ull && static_cast<uint32_t>(sl >> 32) != kl) {
+            il = (il + 1u) & h1.hot_mask;
+            sl = __ldg(h1.hot_slots + il);
+        }
+        if (se == 0ull && sl == 0ull) continue;  // neither value is an exception: the speculation stands
         float ve = fe.v, re = fe.r;
-        const bool se = lif_exact(fe.J, ve, re, dt, tau_rc, tau_ref, p.libm);
+        const bool spk = lif_exact(fe.J, ve, re, dt, tau_rc, tau_ref, p.libm);
         const int64_t o = static_cast<int64_t>(i) * B + b0 + l;
         A[e.v_base + o] = ve;
         A[e.r_base + o] = re;
-        if (last) A[e.out_base + o] = se ? amp_dt : 0.0f;
-        if (se != static_cast<bool>((S.words[i] >> l) & 1u)) atomicXor(S.words + i, 1u << l);
+        if (last) A[e.out_base + o] = spk ? amp_dt : 0.0f;
+        if (spk != static_cast<bool>((S.words[i] >> l) & 1u)) atomicXor(S.words + i, 1u << l);
     }
     __syncthreads();
     tk.tick(FS_FIX);
@@ -352,10 +389,42 @@ __device__ void phase_a_unit(const FusedProgram& p, int unit, bool last, const S
     tk.tick(FS_A3);
 
     // A4: decoders over the spiking neurons of each column, ascending i; the
-    // terms are the precomputed products fp32(D[r,i]) * fp32(amp/dt).  Lanes
-    // are (column, row) with the row fastest, so the rows of one column walk
-    // the same spike list together and each load touches one 32-B sector per
-    // column (products stored transposed, [n][dx]).
+    // terms are the precomputed products fp32(D[r,i]) * fp32(amp/dt), stored
+    // transposed ([n][dx]).  Staged and dx % 4 == 0: lane = column, one warp
+    // per 4 decoded rows, one LDS.128 and four independent sums per spike.
+    if (p.stage_dec && (e.dx & 3) == 0) {
+        const int stride4 = e.dx >> 2;
+        const uint32_t* cw = S.col + lane * p.nwords;
+        for (int g = warp; g < stride4; g += kWarps) {
+            const float4* P4 = reinterpret_cast<const float4*>(S.P) + g;
+            float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+            for (int w = 0; w < nw; ++w) {
+                uint32_t bits = cw[w];
+                while (bits) {
+                    const int i1 = w * 32 + __ffs(bits) - 1;
+                    bits &= bits - 1u;
+                    const float4 t = P4[i1 * stride4];
+                    a0 = a0 + t.x;
+                    a1 = a1 + t.y;
+                    a2 = a2 + t.z;
+                    a3 = a3 + t.w;
+                }
+            }
+            if (valid) {
+                const float* init = p.values + e.xhat_init_off + 4 * g;
+                float* xo = A + e.xhat_base + static_cast<int64_t>(4 * g) * B + b;
+                xo[0] = __ldg(init) + a0;
+                xo[B] = __ldg(init + 1) + a1;
+                xo[2 * B] = __ldg(init + 2) + a2;
+                xo[3 * B] = __ldg(init + 3) + a3;
+            }
+        }
+        __syncthreads();
+        tk.tick(FS_A4);
+        return;
+    }
+    // general layout: lanes are (column, row) with the row fastest, so the
+    // rows of one column walk the same spike list together
     const int rd = e.dx <= 1 ? 1 : 1 << (32 - __clz(e.dx - 1));  // rows per column group (pow2 <= 32)
     for (int idx = threadIdx.x; idx < 32 * rd; idx += kThreads) {
         const int l = idx / rd, rrow = idx - l * rd, bb = b0 + l;
@@ -402,7 +471,12 @@ __device__ __forceinline__ void phase_b_item(const FusedProgram& p, int c, int b
     for (int j = 0; j < DMAX; ++j) x[j] = j < cn.ds ? src[j * B] : 0.0f;
     const float4* T = reinterpret_cast<const float4*>(p.values + cn.tpad_off);
     float* st = A + cn.state_base + b;
-    for (int r = 0; r < cn.dd; ++r) {
+    float s0[DMAX];  // every state load in flight before the arithmetic
+#pragma unroll
+    for (int r = 0; r < DMAX; ++r) s0[r] = r < cn.dd ? st[r * B] : 0.0f;
+#pragma unroll
+    for (int r = 0; r < DMAX; ++r) {
+        if (r >= cn.dd) break;
         float acc = 0.0f;
 #pragma unroll
         for (int q = 0; q < DMAX / 4; ++q) {
@@ -413,7 +487,7 @@ __device__ __forceinline__ void phase_b_item(const FusedProgram& p, int c, int b
             acc = acc + w.w * x[4 * q + 3];
         }
         const float accv = __ldg(p.values + cn.acc_init_off + r) + acc;
-        const float f = cn.a * st[r * B] + cn.b * accv;  // lowpass_step (neuron_math.hpp:39-42)
+        const float f = cn.a * s0[r] + cn.b * accv;  // lowpass_step (neuron_math.hpp:39-42)
         st[r * B] = f;
         if (last) {
             A[cn.acc_base + static_cast<int64_t>(r) * B + b] = accv;

@@ -1,0 +1,47 @@
+"""CPU-only: the C-ABI library loads and exports every entry point declared
+in include/*.h (no device calls)."""
+import ctypes
+import glob
+import os
+import re
+
+from paper_1805_11144_b200 import engine
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        text = open(h).read()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        for m in re.finditer(r"\b(neng_\w+)\s*\(", text):
+            names.add(m.group(1))
+    return sorted(names)
+
+
+def test_headers_declare_the_engine_surface():
+    names = declared_functions()
+    for required in ("neng_gpu_create", "neng_gpu_run", "neng_gpu_reset", "neng_gpu_read_signal",
+                     "neng_gpu_buffer_storage", "neng_gpu_steps_completed", "neng_gpu_destroy",
+                     "neng_gpu_last_error", "neng_run_passes"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = engine.lib()
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_library_is_sm100a():
+    so = engine.LIB_PATH
+    data = open(so, "rb").read()
+    assert b"sm_100a" in data or b"sm_100" in data
+
+
+def test_bad_arguments_fail_with_status_not_crash():
+    lib = engine.lib()
+    out = ctypes.c_void_p()
+    assert lib.neng_gpu_create(None, 1, 1, None, ctypes.byref(out)) == 6  # NENG_INVALID_ARGUMENT
+    assert b"null" in lib.neng_last_error()

@@ -233,3 +233,14 @@ def test_generic_mode_is_forced_and_reported():
     feeds = {node: wave_feed(1, 10, 2, 0.1)}
     assert_bitexact(e.run(10, feeds), ref_run(pm, 1, 10, feeds))
     assert e.last_launch_count() >= 1
+
+
+@pytest.mark.parametrize("name", ["random_seed1", "random_seed2", "random_seed3", "chain", "learning", "lif_drive",
+                                  "ensemble_network"])
+def test_committed_golden_fixtures(name):
+    # fixtures produced by the reference's EngineCore<float> (tests/golden/make_golden.py)
+    import os
+    from tests.golden.make_golden import load_case
+    planned, batch, steps, feeds, probes = load_case(os.path.join(os.path.dirname(__file__), "golden", f"{name}.npz"))
+    for mode in (MODE_GENERIC, 0):
+        assert_bitexact(GpuEngine(planned, batch, mode=mode).run(steps, feeds), probes, f"{name} mode {mode}")
