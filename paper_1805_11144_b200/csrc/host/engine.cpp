@@ -217,6 +217,18 @@ const LibmTables& libm_tables(int device) {
         cuda_check(cudaMemcpy(dreg, reg.data(), reg.size() * 4, cudaMemcpyHostToDevice), "libm regions H2D");
         dl->allocs.push_back(dreg);
         dl->tables.t[t].region_from = static_cast<const float*>(dreg);
+        // screening window of the fast polynomials: the exact window, and never
+        // less than 0.004 ulp (the fast polynomials are within 0.002 ulp)
+        std::vector<uint32_t> win(reg.size());
+        for (size_t i = 0; i < win.size(); ++i) {
+            double w = std::max(0.5 - static_cast<double>(reg[i]), 0.004) * 536870912.0;  // x 2^29
+            win[i] = static_cast<uint32_t>(std::ceil(w));
+        }
+        void* dwin = nullptr;
+        cuda_check(cudaMalloc(&dwin, std::max<size_t>(win.size(), 1) * 4), "cudaMalloc libm windows");
+        cuda_check(cudaMemcpy(dwin, win.data(), win.size() * 4, cudaMemcpyHostToDevice), "libm windows H2D");
+        dl->allocs.push_back(dwin);
+        dl->tables.t[t].region_win = static_cast<const uint32_t*>(dwin);
         dl->tables.t[t].region_shift = ht.region_shift;
         dl->tables.t[t].n_regions = static_cast<uint32_t>(reg.size());
     }

@@ -395,6 +395,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             volatile float mdt = -x.dt, trc = x.tau_rc;
             float arg = mdt / trc;
             x.em_dt = expm1f(arg);  // the host libm result the reference uses
+            x.inv_tau_rc = 1.0 / static_cast<double>(x.tau_rc);
             {
                 // spike products fp32(D[r,i]) * amp_dt: the DotInc term for out[i] = amp/dt
                 const Signal& Ds = m.signals[e.D];

@@ -264,7 +264,10 @@ __device__ void phase_a_unit(const FusedProgram& p, int unit, bool last, const S
             float em = delta == dt ? em_dt : -0.0f;
             bool doubt = false;
             if (live && delta != dt && delta != 0.0f) {
-                const float xa = -delta / tau_rc;
+                // == -delta / tau_rc in IEEE float: the double product is within 2^-52 of the quotient,
+                // and a quotient of floats is never within 2^-49 of a float midpoint unless on it,
+                // which needs a power-of-two divisor (then the product is exact)
+                const float xa = static_cast<float>(static_cast<double>(-delta) * e.inv_tau_rc);
                 if (lif_range(xa)) {
                     const Spec s = spec_lif(xa, false, p.libm);
                     em = s.r;

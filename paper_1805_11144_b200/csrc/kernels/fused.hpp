@@ -32,6 +32,7 @@ struct FEns {
     float dt, tau_rc, tau_ref, amplitude;
     float amp_dt;  // amplitude / dt (the spike value, exec: amplitude / dt)
     float em_dt;   // glibc expm1f(-dt / tau_rc): the refractory-free step
+    double inv_tau_rc;  // 1 / (double)tau_rc
 };
 
 struct FConn {

@@ -72,17 +72,63 @@ __device__ __forceinline__ float region_from(const LibmHash& h, uint32_t key) {
     return __ldg(h.region_from + ((key - 0x80000000u) >> h.region_shift));
 }
 
-/// Speculative evaluation on the LIF range: the double-then-round result and
-/// whether it could be a glibc exception (then the caller must resolve it
-/// exactly, e.g. with glibc_expm1f / glibc_log1pf).
+// ---- the fast screen on the LIF range ----------------------------------
+// Reduced Taylor polynomials, relative error < 2^-33 on [-1/16, 0): far below
+// the screening window, so a value outside the window rounds exactly as the
+// true value does (and as glibc does: every glibc exception lies inside).
+__device__ __forceinline__ double expm1_fast(double x) {  // x + x^2 sum_{k=2..7} x^(k-2)/k!
+    double p = 1.9841269841269841e-04;
+    p = fma(p, x, 1.3888888888888889e-03);
+    p = fma(p, x, 8.3333333333333332e-03);
+    p = fma(p, x, 4.1666666666666664e-02);
+    p = fma(p, x, 1.6666666666666666e-01);
+    p = fma(p, x, 0.5);
+    return fma(x * x, p, x);
+}
+__device__ __forceinline__ double log1p_fast(double x) {  // x + x^2 sum_{k=2..9} (-1)^(k+1) x^(k-2)/k
+    double p = 1.0 / 9.0;
+    p = fma(p, x, -1.0 / 8.0);
+    p = fma(p, x, 1.0 / 7.0);
+    p = fma(p, x, -1.0 / 6.0);
+    p = fma(p, x, 1.0 / 5.0);
+    p = fma(p, x, -1.0 / 4.0);
+    p = fma(p, x, 1.0 / 3.0);
+    p = fma(p, x, -0.5);
+    return fma(x * x, p, x);
+}
+
+/// True when y lies within `win` x 2^-29 float ulps of a float rounding
+/// midpoint (the low 29 mantissa bits of a double are the position between
+/// two consecutive floats of its binade).  Results in the float-denormal
+/// range are always reported (the exact path handles them).
+__device__ __forceinline__ bool in_window(double y, uint32_t win) {
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(y));
+    if (((u >> 52) & 0x7FFull) < 897ull) return true;  // |y| < 2^-126
+    const uint32_t low = static_cast<uint32_t>(u) & 0x1FFFFFFFu;
+    const uint32_t d = low > 0x10000000u ? low - 0x10000000u : 0x10000000u - low;
+    return d <= win;
+}
+
+__device__ __forceinline__ uint32_t region_win(const LibmHash& h, uint32_t key) {
+    return __ldg(h.region_win + ((key - 0x80000000u) >> h.region_shift));
+}
+
+/// Speculative evaluation on the LIF range: the value glibc returns unless
+/// `doubtful` (then resolve exactly with glibc_expm1f / glibc_log1pf).
 struct Spec {
     float r;
     bool doubtful;
 };
+__device__ __forceinline__ Spec spec_expm1(float x, const LibmTables& t) {
+    const double y = expm1_fast(static_cast<double>(x));
+    return {static_cast<float>(y), in_window(y, region_win(t.t[0], __float_as_uint(x)))};
+}
+__device__ __forceinline__ Spec spec_log1p(float x, const LibmTables& t) {
+    const double y = log1p_fast(static_cast<double>(x));
+    return {static_cast<float>(y), in_window(y, region_win(t.t[1], __float_as_uint(x)))};
+}
 __device__ __forceinline__ Spec spec_lif(float x, bool is_log, const LibmTables& t) {
-    const double y = small_f(static_cast<double>(x), is_log);
-    const LibmHash& h = is_log ? t.t[1] : t.t[0];
-    return {static_cast<float>(y), near_midpoint(y, region_from(h, __float_as_uint(x)))};
+    return is_log ? spec_log1p(x, t) : spec_expm1(x, t);
 }
 
 /// glibc expm1f.
@@ -90,6 +136,8 @@ __device__ __forceinline__ float glibc_expm1f(float x, const LibmTables& t) {
     if (x == 0.0f) return x;  // expm1(+-0) = +-0 exactly
     const uint32_t k = __float_as_uint(x);
     if (lif_range(x)) {
+        const Spec s = spec_expm1(x, t);
+        if (!s.doubtful) return s.r;
         const double y = small_f(static_cast<double>(x), false);
         const float r = static_cast<float>(y);
         return near_midpoint(y, region_from(t.t[0], k))
@@ -108,6 +156,8 @@ __device__ __forceinline__ float glibc_log1pf(float x, const LibmTables& t) {
     if (x == 0.0f) return x;
     const uint32_t k = __float_as_uint(x);
     if (lif_range(x)) {
+        const Spec s = spec_log1p(x, t);
+        if (!s.doubtful) return s.r;
         const double y = small_f(static_cast<double>(x), true);
         const float r = static_cast<float>(y);
         return near_midpoint(y, region_from(t.t[1], k))

@@ -81,6 +81,7 @@ struct LibmHash {
     int32_t hot_shift = 32;
     // per-region bounds on [-1/16, 0): region = (key - 0x80000000) >> region_shift
     const float* region_from = nullptr;
+    const uint32_t* region_win = nullptr;  // screening half-window per region, units of 2^-29 float ulp
     uint32_t region_shift = 31;
     uint32_t n_regions = 0;
 };
