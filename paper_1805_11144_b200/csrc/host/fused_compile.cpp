@@ -374,12 +374,14 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             push_values(m.operators[e.rj].value);
             while (static_cast<int64_t>(values.size()) < x.bias_off + x.n_pad) values.push_back(0.0f);
             {
-                // encoder rows zero padded to DMAX (exact: see fused.cu)
+                // encoder rows zero padded to DMAX (exact: see fused.cu), n rounded
+                // up to even with a zero row (phase A takes neurons in pairs)
                 const Signal& Es = m.signals[e.E];
                 x.epad_off = align4();
-                for (int ii = 0; ii < x.n; ++ii)
+                const int n2 = (x.n + 1) & ~1;
+                for (int ii = 0; ii < n2; ++ii)
                     for (int jj = 0; jj < DMAX; ++jj)
-                        values.push_back(jj < x.d && !Es.initial.empty()
+                        values.push_back(ii < x.n && jj < x.d && !Es.initial.empty()
                                              ? static_cast<float>(Es.initial[static_cast<size_t>(ii) * x.d + jj])
                                              : 0.0f);
             }

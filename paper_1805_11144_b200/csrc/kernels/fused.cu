@@ -155,22 +155,32 @@ __device__ __forceinline__ bool lif_exact(float J, float& v, float& r, float dt,
     return false;
 }
 
-template <int DMAX, bool PROF>
+/// The batch width: BT when the kernel is specialised for it (row strides then
+/// fold into load/store immediates), else the program's.
+template <int BT>
+__device__ __forceinline__ int batch_of(const FusedProgram& p) {
+    if constexpr (BT > 0)
+        return BT;
+    else
+        return p.batch;
+}
+
+template <int DMAX, int BT, bool PROF>
 __device__ void phase_a_unit(const FusedProgram& p, int unit, bool last, const Smem& S, uint32_t parity,
                              Ticker<PROF>& tk) {
-    const int B = p.batch;
+    const int B = batch_of<BT>(p);
     const int t = unit / p.btiles;
     const int b0 = (unit - t * p.btiles) * 32;
     const FEns& e = p.ens[t];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int b = b0 + lane;
-    const bool valid = b < B;
+    const bool valid = (BT > 0 && BT % 32 == 0) || b < B;
     float* A = p.arena;
 
     // stage encoders, biases and decoder products (async; overlaps A1)
     if (threadIdx.x == 0) {
         fence_proxy_async_smem();  // prior generic accesses of the staging buffers are ordered first
-        const uint32_t eb = static_cast<uint32_t>(e.n) * DMAX * 4, bb = static_cast<uint32_t>(e.n_pad) * 4;
+        const uint32_t eb = static_cast<uint32_t>((e.n + 1) & ~1) * DMAX * 4, bb = static_cast<uint32_t>(e.n_pad) * 4;
         const uint32_t pb = p.stage_dec ? static_cast<uint32_t>(e.dec_bytes) : 0u;
         mbar_expect_tx(S.bar, eb + bb + pb);
         bulk_g2s(S.E, p.values + e.epad_off, eb, S.bar);
@@ -211,114 +221,143 @@ __device__ void phase_a_unit(const FusedProgram& p, int unit, bool last, const S
     mbar_wait(S.bar, parity);
     tk.tick(FS_A1);
 
-    // A2: encoder + lif_spike_step<float> (neuron_math.hpp:55-77), speculative transcendentals
+    // A2: encoder + lif_spike_step<float> (neuron_math.hpp:55-77), speculative transcendentals.
+    // Neurons go in pairs through the paired fp32 pipe (FADD2/FMUL2: two IEEE
+    // round-to-nearest operations per instruction, bit-identical to scalar ones);
+    // the rarely taken transcendental branches stay scalar.
     const float dt = e.dt, tau_rc = e.tau_rc, tau_ref = e.tau_ref, amp_dt = e.amp_dt, em_dt = e.em_dt;
     const int npw = ((e.n + kWarps - 1) / kWarps + kUnroll - 1) / kUnroll * kUnroll;
     const int nbeg = warp * npw, nend = min(e.n, nbeg + npw);
-    float* vcol = A + e.v_base + b;
-    float* rcol = A + e.r_base + b;
+    float* vp = A + e.v_base + b + static_cast<int64_t>(nbeg) * B;  // row i0 of the current round
+    float* rp = A + e.r_base + b + static_cast<int64_t>(nbeg) * B;
+    const float2 dt2 = make_float2(dt, dt), ndt2 = make_float2(-dt, -dt);
     float vnx[kUnroll], rnx[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-        const int i = nbeg + u;
         vnx[u] = rnx[u] = 0.f;
-        if (i < nend && valid) {
-            vnx[u] = __ldcs(vcol + i * B);
-            rnx[u] = __ldcs(rcol + i * B);
+        if (nbeg + u < nend && valid) {
+            vnx[u] = __ldcs(vp + u * B);
+            rnx[u] = __ldcs(rp + u * B);
         }
     }
-    for (int i0 = nbeg; i0 < nend; i0 += kUnroll) {
+    for (int i0 = nbeg; i0 < nend; i0 += kUnroll, vp += kUnroll * B, rp += kUnroll * B) {
         float v[kUnroll], r[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             v[u] = vnx[u];
             r[u] = rnx[u];
-            const int i = i0 + kUnroll + u;  // prefetch the next round
             vnx[u] = rnx[u] = 0.f;
-            if (i < nend && valid) {
-                vnx[u] = __ldcs(vcol + i * B);
-                rnx[u] = __ldcs(rcol + i * B);
+            if (i0 + kUnroll + u < nend && valid) {  // prefetch the next round
+                vnx[u] = __ldcs(vp + (kUnroll + u) * B);
+                rnx[u] = __ldcs(rp + (kUnroll + u) * B);
             }
         }
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const int i = i0 + u;
+        for (int k = 0; k < kUnroll / 2; ++k) {
+            const int i = i0 + 2 * k;
             if (i >= nend) break;  // warp-uniform
-            const bool live = valid;
-            // DotInc(E, in, J): acc from +0, j ascending, then J = bias + acc
-            const float4* er = reinterpret_cast<const float4*>(S.E + i * DMAX);
-            float acc = 0.0f;
+            // DotInc(E, in, J) for neurons i, i+1: acc from +0, j ascending, then J = bias + acc.
+            // Products two dims at a time (FMUL2), sums scalar and in order.  A
+            // paired product must never feed a paired sum: ptxas contracts
+            // FMUL2 -> FADD2 into FFMA2 even for .rn (tests/test_abi.py checks the SASS).
+            float acc[2];
 #pragma unroll
-            for (int q = 0; q < DMAX / 4; ++q) {
-                const float4 w = er[q];
-                acc = acc + w.x * x[4 * q];
-                acc = acc + w.y * x[4 * q + 1];
-                acc = acc + w.z * x[4 * q + 2];
-                acc = acc + w.w * x[4 * q + 3];
+            for (int h = 0; h < 2; ++h) {
+                const float4* er = reinterpret_cast<const float4*>(S.E + (i + h) * DMAX);
+                float a = 0.0f;
+#pragma unroll
+                for (int q = 0; q < DMAX / 4; ++q) {
+                    const float4 w = er[q];
+                    const float2 m0 = __fmul2_rn(make_float2(w.x, w.y), make_float2(x[4 * q], x[4 * q + 1]));
+                    const float2 m1 = __fmul2_rn(make_float2(w.z, w.w), make_float2(x[4 * q + 2], x[4 * q + 3]));
+                    a = a + m0.x;
+                    a = a + m0.y;
+                    a = a + m1.x;
+                    a = a + m1.y;
+                }
+                acc[h] = a;
             }
-            const float J = S.bias[i] + acc;
-            float delta = dt - r[u];
-            if (delta < 0.0f) delta = 0.0f;
-            if (delta > dt) delta = dt;
-            // expm1(-delta/tau_rc): delta == dt -> the host glibc value; delta == +0 -> expm1(-0) = -0
-            float em = delta == dt ? em_dt : -0.0f;
-            bool doubt = false;
-            if (live && delta != dt && delta != 0.0f) {
-                // == -delta / tau_rc in IEEE float: the double product is within 2^-52 of the quotient,
-                // and a quotient of floats is never within 2^-49 of a float midpoint unless on it,
-                // which needs a power-of-two divisor (then the product is exact)
-                const float xa = static_cast<float>(static_cast<double>(-delta) * e.inv_tau_rc);
-                if (lif_range(xa)) {
-                    const Spec s = spec_lif(xa, false, p.libm);
-                    em = s.r;
-                    doubt = s.doubtful;
+            const float2 J2 = __fadd2_rn(*reinterpret_cast<const float2*>(S.bias + i), make_float2(acc[0], acc[1]));
+            const float2 v2 = make_float2(v[2 * k], v[2 * k + 1]), r2 = make_float2(r[2 * k], r[2 * k + 1]);
+            const float2 dl2 = __fadd2_rn(dt2, make_float2(-r2.x, -r2.y));  // dt - r
+            const float2 rr2 = __fadd2_rn(r2, ndt2);                        // r - dt
+            float em[2];
+            bool doubt[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float delta = h ? dl2.y : dl2.x;
+                if (delta < 0.0f) delta = 0.0f;
+                if (delta > dt) delta = dt;
+                // expm1(-delta/tau_rc): delta == dt -> the host glibc value; delta == +0 -> expm1(-0) = -0
+                em[h] = delta == dt ? em_dt : -0.0f;
+                doubt[h] = false;
+                if (valid && delta != dt && delta != 0.0f) {
+                    // == -delta / tau_rc in IEEE float: the double product is within 2^-52 of the quotient,
+                    // and a quotient of floats is never within 2^-49 of a float midpoint unless on it,
+                    // which needs a power-of-two divisor (then the product is exact)
+                    const float xa = static_cast<float>(static_cast<double>(-delta) * e.inv_tau_rc);
+                    if (lif_range(xa)) {
+                        const Spec s = spec_lif(xa, false, p.libm);
+                        em[h] = s.r;
+                        doubt[h] = s.doubtful;
+                    } else {
+                        em[h] = glibc_expm1f(xa, p.libm);
+                    }
+                }
+            }
+            // v - (J - v) * em: scalar products between the paired sums (see above)
+            const float2 d2 = __fadd2_rn(J2, make_float2(-v2.x, -v2.y));
+            const float t0 = __fmul_rn(d2.x, em[0]), t1 = __fmul_rn(d2.y, em[1]);
+            const float2 vn2 = __fadd2_rn(v2, make_float2(-t0, -t1));
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (h && i + 1 >= nend) break;  // warp-uniform
+                const float J = h ? J2.y : J2.x, vh = h ? v2.y : v2.x, rh = h ? r2.y : r2.x;
+                float vn = h ? vn2.y : vn2.x;
+                if (vn < 0.0f) vn = 0.0f;
+                const bool spike = valid && vn > 1.0f;
+                bool dbt = doubt[h];
+                float vo, ro;
+                if (spike) {
+                    const float xl = -(vn - 1.0f) / (J - 1.0f);
+                    float lg;
+                    if (lif_range(xl)) {
+                        const Spec s = spec_lif(xl, true, p.libm);
+                        lg = s.r;
+                        dbt = dbt || s.doubtful;
+                    } else {
+                        lg = glibc_log1pf(xl, p.libm);
+                    }
+                    const float since = -tau_rc * lg;
+                    vo = 0.0f;
+                    ro = tau_ref - since;
                 } else {
-                    em = glibc_expm1f(xa, p.libm);
+                    vo = vn;
+                    ro = rh > dt ? (h ? rr2.y : rr2.x) : 0.0f;
                 }
-            }
-            float vn = v[u] - (J - v[u]) * em;
-            if (vn < 0.0f) vn = 0.0f;
-            const bool spike = live && vn > 1.0f;
-            float vo, ro;
-            if (spike) {
-                const float xl = -(vn - 1.0f) / (J - 1.0f);
-                float lg;
-                if (lif_range(xl)) {
-                    const Spec s = spec_lif(xl, true, p.libm);
-                    lg = s.r;
-                    doubt = doubt || s.doubtful;
-                } else {
-                    lg = glibc_log1pf(xl, p.libm);
+                bool spike_final = spike;
+                if (dbt) {  // queue the neuron for exact resolution from its original inputs
+                    const int slot = atomicAdd(S.nfix, 1);
+                    if (slot < kFixCap) {
+                        S.fix[slot] = {((i + h) << 5) | lane, vh, rh, J};
+                    } else {  // queue full: resolve right here
+                        float ve = vh, re = rh;
+                        spike_final = lif_exact(J, ve, re, dt, tau_rc, tau_ref, p.libm);
+                        vo = ve;
+                        ro = re;
+                    }
                 }
-                const float since = -tau_rc * lg;
-                vo = 0.0f;
-                ro = tau_ref - since;
-            } else {
-                vo = vn;
-                ro = r[u] > dt ? r[u] - dt : 0.0f;
-            }
-            bool spike_final = spike;
-            if (doubt) {  // queue the neuron for exact resolution from its original inputs
-                const int slot = atomicAdd(S.nfix, 1);
-                if (slot < kFixCap) {
-                    S.fix[slot] = {(i << 5) | lane, v[u], r[u], J};
-                } else {  // queue full: resolve right here
-                    float ve = v[u], re = r[u];
-                    spike_final = lif_exact(J, ve, re, dt, tau_rc, tau_ref, p.libm);
-                    vo = ve;
-                    ro = re;
+                const uint32_t word = __ballot_sync(0xffffffffu, spike_final);
+                if (valid) {
+                    __stcs(vp + (2 * k + h) * B, vo);
+                    __stcs(rp + (2 * k + h) * B, ro);
+                    if (last) {
+                        A[e.j_base + static_cast<int64_t>(i + h) * B + b] = J;
+                        A[e.out_base + static_cast<int64_t>(i + h) * B + b] = spike_final ? amp_dt : 0.0f;
+                    }
                 }
+                if (lane == 0) S.words[i + h] = word;
             }
-            const uint32_t word = __ballot_sync(0xffffffffu, spike_final);
-            if (valid) {
-                __stcs(vcol + i * B, vo);
-                __stcs(rcol + i * B, ro);
-                if (last) {
-                    A[e.j_base + static_cast<int64_t>(i) * B + b] = J;
-                    A[e.out_base + static_cast<int64_t>(i) * B + b] = spike_final ? amp_dt : 0.0f;
-                }
-            }
-            if (lane == 0) S.words[i] = word;
         }
     }
     __syncthreads();
@@ -458,9 +497,9 @@ __device__ void phase_a_unit(const FusedProgram& p, int unit, bool last, const S
     tk.tick(FS_A4);
 }
 
-template <int DMAX>
+template <int DMAX, int BT>
 __device__ __forceinline__ void phase_b_item(const FusedProgram& p, int c, int b, bool last, int ks) {
-    const int B = p.batch;
+    const int B = batch_of<BT>(p);
     const FConn& cn = p.conns[c];
     float* A = p.arena;
     float x[DMAX];
@@ -534,7 +573,7 @@ size_t smem_bytes(const FusedProgram& p) {
            static_cast<size_t>(p.nmax) * 4 + static_cast<size_t>(32) * p.nwords * 4 + sizeof(FixEntry) * kFixCap;
 }
 
-template <int DMAX, bool PROF>
+template <int DMAX, int BT, bool PROF>
 __global__ void __launch_bounds__(kThreads, 3) fused_run_kernel(FusedProgram p, int k_begin, int k_end) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(128) uint32_t smem[];
@@ -542,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 3) fused_run_kernel(FusedProgram p, 
     if (threadIdx.x == 0) mbar_init(S.bar);
     __syncthreads();
     uint32_t parity = 0;
-    const int B = p.batch;
+    const int B = batch_of<BT>(p);
     const int units = p.n_ens * p.btiles;
     const int64_t gthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
     const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -572,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, 3) fused_run_kernel(FusedProgram p, 
             __syncthreads();
             const int u = *S.next_unit;
             if (u >= units) break;  // uniform; the next write of next_unit follows a barrier inside the unit
-            phase_a_unit<DMAX, PROF>(p, u, last, S, parity, tk);
+            phase_a_unit<DMAX, BT, PROF>(p, u, last, S, parity, tk);
             parity ^= 1u;
         }
         grid_sync(grid);
@@ -583,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, 3) fused_run_kernel(FusedProgram p, 
         const int64_t items = static_cast<int64_t>(p.n_conn) * B;
         for (int64_t it = gtid; it < items; it += gthreads) {
             const int c = static_cast<int>(it / B);
-            phase_b_item<DMAX>(p, c, static_cast<int>(it - static_cast<int64_t>(c) * B), last, k);
+            phase_b_item<DMAX, BT>(p, c, static_cast<int>(it - static_cast<int64_t>(c) * B), last, k);
         }
         for (int q = 0; q < p.n_probes; ++q) {
             const FProbe& pr = p.probes[q];
@@ -615,33 +654,56 @@ __global__ void __launch_bounds__(kThreads, 3) fused_run_kernel(FusedProgram p, 
     tk.flush(p.prof);
 }
 
-template <int DMAX, bool PROF>
+template <int DMAX, int BT, bool PROF>
 cudaError_t launch_t(const FusedProgram& p, int grid, int k0, int k1, cudaStream_t stream) {
     size_t sm = smem_bytes<DMAX>(p);
     if (sm > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(fused_run_kernel<DMAX, PROF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(sm));
+        cudaError_t e = cudaFuncSetAttribute(fused_run_kernel<DMAX, BT, PROF>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
         if (e != cudaSuccess) return e;
     }
     FusedProgram prog = p;
     void* args[] = {&prog, &k0, &k1};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fused_run_kernel<DMAX, PROF>), dim3(grid),
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fused_run_kernel<DMAX, BT, PROF>), dim3(grid),
                                        dim3(kThreads), args, sm, stream);
 }
 
-template <int DMAX>
+template <int DMAX, int BT>
 int max_grid_t(const FusedProgram& p, int device) {
     size_t sm = smem_bytes<DMAX>(p);
     if (sm > 227 * 1024) return 0;
     if (sm > 48 * 1024) {
-        cudaFuncSetAttribute(fused_run_kernel<DMAX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-        cudaFuncSetAttribute(fused_run_kernel<DMAX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+        cudaFuncSetAttribute(fused_run_kernel<DMAX, BT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sm));
+        cudaFuncSetAttribute(fused_run_kernel<DMAX, BT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sm));
     }
     int per_sm = 0, per_sm_prof = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_run_kernel<DMAX, false>, kThreads, sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_prof, fused_run_kernel<DMAX, true>, kThreads, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_run_kernel<DMAX, BT, false>, kThreads, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_prof, fused_run_kernel<DMAX, BT, true>, kThreads, sm);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     return (per_sm < per_sm_prof ? per_sm : per_sm_prof) * sms;
+}
+
+// Batch widths with a stride-specialised kernel (others run the runtime-stride one).
+#define NENG_FUSED_BATCHES(X) X(32) X(256)
+
+template <int DMAX, bool PROF>
+cudaError_t launch_d(const FusedProgram& p, int grid, int k0, int k1, cudaStream_t stream) {
+#define NENG_CASE(BB) \
+    if (p.batch == BB) return launch_t<DMAX, BB, PROF>(p, grid, k0, k1, stream);
+    NENG_FUSED_BATCHES(NENG_CASE)
+#undef NENG_CASE
+    return launch_t<DMAX, 0, PROF>(p, grid, k0, k1, stream);
+}
+
+template <int DMAX>
+int max_grid_d(const FusedProgram& p, int device) {
+#define NENG_CASE(BB) \
+    if (p.batch == BB) return max_grid_t<DMAX, BB>(p, device);
+    NENG_FUSED_BATCHES(NENG_CASE)
+#undef NENG_CASE
+    return max_grid_t<DMAX, 0>(p, device);
 }
 
 }  // namespace
@@ -651,18 +713,18 @@ int fused_dmax_for(int d) { return d <= 8 ? 8 : d <= 16 ? 16 : d <= 32 ? 32 : 0;
 cudaError_t launch_fused(const FusedProgram& p, int dmax, int grid, int k0, int k1, cudaStream_t stream) {
     const bool prof = p.prof != nullptr;
     switch (dmax) {
-        case 8: return prof ? launch_t<8, true>(p, grid, k0, k1, stream) : launch_t<8, false>(p, grid, k0, k1, stream);
-        case 16: return prof ? launch_t<16, true>(p, grid, k0, k1, stream) : launch_t<16, false>(p, grid, k0, k1, stream);
-        case 32: return prof ? launch_t<32, true>(p, grid, k0, k1, stream) : launch_t<32, false>(p, grid, k0, k1, stream);
+        case 8: return prof ? launch_d<8, true>(p, grid, k0, k1, stream) : launch_d<8, false>(p, grid, k0, k1, stream);
+        case 16: return prof ? launch_d<16, true>(p, grid, k0, k1, stream) : launch_d<16, false>(p, grid, k0, k1, stream);
+        case 32: return prof ? launch_d<32, true>(p, grid, k0, k1, stream) : launch_d<32, false>(p, grid, k0, k1, stream);
     }
     return cudaErrorInvalidValue;
 }
 
 int fused_max_grid(const FusedProgram& p, int dmax, int device) {
     switch (dmax) {
-        case 8: return max_grid_t<8>(p, device);
-        case 16: return max_grid_t<16>(p, device);
-        case 32: return max_grid_t<32>(p, device);
+        case 8: return max_grid_d<8>(p, device);
+        case 16: return max_grid_d<16>(p, device);
+        case 32: return max_grid_d<32>(p, device);
     }
     return 0;
 }

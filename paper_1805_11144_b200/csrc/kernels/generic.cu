@@ -302,7 +302,10 @@ __global__ void libm_eval_kernel(int func, uint32_t lo, int64_t n, uint32_t* out
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         float x = __uint_as_float(static_cast<uint32_t>(lo + i));
-        float r = func == 0 ? glibc_expm1f(x, t) : glibc_log1pf(x, t);
+        // 0/1: expm1f/log1pf; 2/3: the same through the fused kernel's speculate-and-resolve path
+        float r = func == 0   ? glibc_expm1f(x, t)
+                  : func == 1 ? glibc_log1pf(x, t)
+                              : glibc_spec_resolved(x, func == 3, t);
         out[i] = __float_as_uint(r);
     }
 }

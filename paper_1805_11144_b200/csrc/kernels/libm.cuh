@@ -15,6 +15,7 @@
 // host, bit for bit.
 #pragma once
 
+#include "libm_fast.h"
 #include "program.hpp"
 
 namespace nengb {
@@ -73,29 +74,14 @@ __device__ __forceinline__ float region_from(const LibmHash& h, uint32_t key) {
 }
 
 // ---- the fast screen on the LIF range ----------------------------------
-// Reduced Taylor polynomials, relative error < 2^-33 on [-1/16, 0): far below
-// the screening window, so a value outside the window rounds exactly as the
-// true value does (and as glibc does: every glibc exception lies inside).
-__device__ __forceinline__ double expm1_fast(double x) {  // x + x^2 sum_{k=2..7} x^(k-2)/k!
-    double p = 1.9841269841269841e-04;
-    p = fma(p, x, 1.3888888888888889e-03);
-    p = fma(p, x, 8.3333333333333332e-03);
-    p = fma(p, x, 4.1666666666666664e-02);
-    p = fma(p, x, 1.6666666666666666e-01);
-    p = fma(p, x, 0.5);
-    return fma(x * x, p, x);
-}
-__device__ __forceinline__ double log1p_fast(double x) {  // x + x^2 sum_{k=2..9} (-1)^(k+1) x^(k-2)/k
-    double p = 1.0 / 9.0;
-    p = fma(p, x, -1.0 / 8.0);
-    p = fma(p, x, 1.0 / 7.0);
-    p = fma(p, x, -1.0 / 6.0);
-    p = fma(p, x, 1.0 / 5.0);
-    p = fma(p, x, -1.0 / 4.0);
-    p = fma(p, x, 1.0 / 3.0);
-    p = fma(p, x, -0.5);
-    return fma(x * x, p, x);
-}
+// Reduced Taylor polynomials (libm_fast.h), relative error < 3e-11 on
+// [-1/16, 0): far below the screening window, so a value outside the window
+// rounds exactly as the true value does (and as glibc does: every glibc
+// exception lies inside).  Inside the window the rounded polynomial value is
+// glibc's unless the input is in the table: the generator records every
+// LIF-range input where the two differ, exceptions or not.
+__device__ __forceinline__ double expm1_fast(double x) { return neng_expm1_fast(x); }
+__device__ __forceinline__ double log1p_fast(double x) { return neng_log1p_fast(x); }
 
 /// True when y lies within `win` x 2^-29 float ulps of a float rounding
 /// midpoint (the low 29 mantissa bits of a double are the position between
@@ -172,6 +158,29 @@ __device__ __forceinline__ float glibc_log1pf(float x, const LibmTables& t) {
         if (near_midpoint(y, t.t[2].lookup_from)) return probe_slots(t.t[2].slots, t.t[2].mask, t.t[2].shift, k, r);
     }
     return r;  // x < -1: NaN; -1: -inf; +inf: +inf; NaN: NaN
+}
+
+/// Whether key is listed in the LIF-range table (an exception, or an input
+/// where the speculative polynomial rounds differently from glibc).
+__device__ __forceinline__ bool hot_listed(const LibmHash& h, uint32_t key) {
+    uint32_t i = (key * 0x9E3779B1u) >> h.hot_shift;
+    for (;;) {
+        const unsigned long long s = __ldg(h.hot_slots + i);
+        if (s == 0ull) return false;
+        if (static_cast<uint32_t>(s >> 32) == key) return true;
+        i = (i + 1u) & h.hot_mask;
+    }
+}
+
+/// The fused kernel's resolution of a value (fused.cu, A2 fix-up): on the LIF
+/// range the speculation stands unless it is doubtful AND x is table-listed,
+/// then the exact path decides.  Equal to glibc for every float (exhaustive test).
+__device__ __forceinline__ float glibc_spec_resolved(float x, bool is_log, const LibmTables& t) {
+    if (lif_range(x)) {
+        const Spec s = spec_lif(x, is_log, t);
+        if (!s.doubtful || !hot_listed(t.t[is_log ? 1 : 0], __float_as_uint(x))) return s.r;
+    }
+    return is_log ? glibc_log1pf(x, t) : glibc_expm1f(x, t);
 }
 
 /// lif_spike_step<float> (neuron_math.hpp:55-77), operation for operation.

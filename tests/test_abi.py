@@ -40,6 +40,24 @@ def test_library_is_sm100a():
     assert b"sm_100a" in data or b"sm_100" in data
 
 
+def test_no_contracted_paired_fma_in_sass():
+    """Bit parity needs every product rounded before its sum.  The kernels are
+    built with -fmad=false, but ptxas still contracts a paired multiply feeding
+    a paired add (mul.rn.f32x2 -> add.rn.f32x2) into FFMA2, so the code never
+    chains them; this keeps it that way."""
+    import shutil
+    import subprocess
+
+    import pytest
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", engine.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    assert "fused_run_kernel" in sass
+    assert not re.search(r"\bFFMA2\b", sass)
+
+
 def test_bad_arguments_fail_with_status_not_crash():
     lib = engine.lib()
     out = ctypes.c_void_p()

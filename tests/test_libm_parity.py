@@ -28,7 +28,7 @@ def _host_lib():
     return lib
 
 
-def _compare(table, func, lo, hi, chunk=1 << 27):
+def _compare(table, func, lo, hi, chunk=1 << 27, device_func=None):
     host = _host_lib()
     threads = os.cpu_count() or 8
     buf = np.zeros(chunk, dtype=np.uint32)
@@ -36,7 +36,7 @@ def _compare(table, func, lo, hi, chunk=1 << 27):
     at = lo
     while at <= hi:
         n = min(chunk, hi - at + 1)
-        dev = passes.debug_libm_eval(func, at, n)
+        dev = passes.debug_libm_eval(func if device_func is None else device_func, at, n)
         host.nlibm_eval(func, at, n, buf.ctypes.data_as(C.POINTER(C.c_uint32)), threads)
         h = buf[:n]
         keys = np.arange(at, at + n, dtype=np.uint64).astype(np.uint32)
@@ -61,6 +61,15 @@ def test_libm_parity_exhaustive():
             for t, k in allbad:
                 f.write(f"{t} {k:08x}\n")
     assert not allbad, f"{len(allbad)} device/host libm mismatches (first: {allbad[:5]})"
+
+
+def test_speculative_resolution_whole_lif_range():
+    """The fused kernel accepts a speculative (reduced-polynomial) value on the
+    LIF range unless it is doubtful and table-listed (glibc_spec_resolved, the
+    semantics of fused.cu's fix-up).  Every float of [-1/16, 0), both functions."""
+    bad = _compare(0, 0, 0x80000001, 0xBD800000, device_func=2)
+    bad += _compare(1, 1, 0x80000001, 0xBD800000, device_func=3)
+    assert not bad, bad[:10]
 
 
 def test_libm_parity_lif_hot_range():
