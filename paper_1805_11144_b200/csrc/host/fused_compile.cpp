@@ -35,6 +35,7 @@
 namespace nengb {
 
 int fused_dmax_for(int d);
+size_t fused_smem_bytes(const FusedProgram& p, int dmax);
 cudaError_t launch_fused(const FusedProgram& p, int dmax, int grid, int k0, int k1, cudaStream_t stream);
 int fused_max_grid(const FusedProgram& p, int dmax, int device);
 
@@ -54,7 +55,7 @@ class FusedImpl : public FusedPlan {
   public:
     FusedProgram prog;
     int dmax = 8, grid = 1, steps_per_launch = 0;
-    DevMem d_ens, d_conns, d_incoming, d_values, d_probes, d_feeds, d_call, d_prof, d_work;
+    DevMem d_ens, d_conns, d_incoming, d_orphans, d_values, d_probes, d_feeds, d_call, d_prof, d_work, d_xbuf;
     std::string desc;
 
     int64_t run(int n_steps, const float* d_feed_data, const int64_t* feed_off, const int* present, float* d_ring,
@@ -76,8 +77,8 @@ class FusedImpl : public FusedPlan {
         p.call_steps = n_steps;
         const bool profile = std::getenv("NENG_FUSED_PROFILE") != nullptr;
         if (profile) {
-            d_prof.ensure(FS_COUNT * 8);
-            cuda_check(cudaMemsetAsync(d_prof.p, 0, FS_COUNT * 8, stream), "profile reset");
+            d_prof.ensure((FS_COUNT + 4) * 8);
+            cuda_check(cudaMemsetAsync(d_prof.p, 0, (FS_COUNT + 4) * 8, stream), "profile reset");
             p.prof = d_prof.as<unsigned long long>();
         }
         d_work.ensure(16);
@@ -91,16 +92,19 @@ class FusedImpl : public FusedPlan {
         }
         cuda_check(cudaStreamSynchronize(stream), "fused run");  // call tables are reused next call
         if (profile) {
-            unsigned long long h[FS_COUNT];
+            unsigned long long h[FS_COUNT + 4];
             cuda_check(cudaMemcpy(h, d_prof.p, sizeof h, cudaMemcpyDeviceToHost), "profile D2H");
-            static const char* names[FS_COUNT] = {"feed",      "A1 in+stage", "A2 lif", "A2 fixup", "A3 transpose",
-                                                  "A4 decode", "barrier1",    "B conn", "barrier2"};
+            static const char* names[FS_COUNT] = {"deferred", "in+conn", "sweep", "queue", "fixup",
+                                                  "decode",   "barrier", "epilogue"};
             double tot = 0;
-            for (unsigned long long x : h) tot += static_cast<double>(x);
+            for (int s = 0; s < FS_COUNT; ++s) tot += static_cast<double>(h[s]);
             std::fprintf(stderr, "[fused profile] %d steps, grid %d: per-step per-CTA us:", n_steps, grid);
             for (int s = 0; s < FS_COUNT; ++s)
                 std::fprintf(stderr, " %s=%.1f", names[s], h[s] / 1e3 / grid / n_steps);
             std::fprintf(stderr, " (total %.1f)\n", tot / 1e3 / grid / n_steps);
+            std::fprintf(stderr, "[fused profile] per step: exit batches %.0f, spike batches %.0f, doubt batches %.0f, doubt entries %.0f\n",
+                         double(h[FS_COUNT]) / n_steps, double(h[FS_COUNT + 1]) / n_steps, double(h[FS_COUNT + 2]) / n_steps,
+                         double(h[FS_COUNT + 3]) / n_steps);
         }
         return launches;
     }
@@ -339,8 +343,8 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         FusedProgram& p = impl->prog;
         const float dt = static_cast<float>(m.dt);
         std::vector<FEns> fe;
-        std::vector<int64_t> incoming;
-        int nmax = 0, dmax_need = 1, pmax_floats = 0;
+        std::vector<int32_t> incoming, orphans;
+        int nmax = 0, dmax_need = 1, pmax_floats = 0, xrows = 0;
         for (const EnsInfo& e : ens)
             dmax_need = std::max({dmax_need, m.signals[e.in].rows(), m.signals[e.xhat].rows()});
         for (const ConnInfo& c : conns)
@@ -361,13 +365,11 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             x.v_base = eng.resolve_full(e.v).base;
             x.r_base = eng.resolve_full(e.r).base;
             x.xhat_base = eng.resolve_full(e.xhat).base;
-            x.enc_base = eng.resolve_full(e.E).base;
-            x.dec_base = eng.resolve_full(e.D).base;
             x.n = m.signals[e.j].rows();
             x.d = m.signals[e.in].rows();
             x.dx = m.signals[e.xhat].rows();
             x.inc_begin = static_cast<int32_t>(incoming.size());
-            for (auto [g, ci] : e.incs) incoming.push_back(eng.resolve_full(conns[conn_of_copy.at(ci)].state).base);
+            for (auto [g, ci] : e.incs) incoming.push_back(conn_of_copy.at(ci));
             x.inc_count = static_cast<int32_t>(e.incs.size());
             x.n_pad = (x.n + 3) / 4 * 4;
             x.bias_off = align4();
@@ -387,6 +389,8 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             }
             x.in_init_off = push_values(m.operators[e.rin].value);
             x.xhat_init_off = push_values(m.operators[e.rx].value);
+            x.xb_row = xrows;
+            xrows += x.dx;
             const NeuronModel& nm = m.operators[e.sn].neuron;
             x.dt = dt;
             x.tau_rc = static_cast<float>(nm.tau_rc);
@@ -419,13 +423,14 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         for (const ConnInfo& c : conns) {
             FConn x{};
             x.src_base = eng.resolve_full(c.src).base;
-            x.t_base = eng.resolve_full(c.T).base;
             x.acc_base = eng.resolve_full(c.accs).base;
             x.filt_base = eng.resolve_full(c.filt).base;
             x.state_base = eng.resolve_full(c.state).base;
             x.dd = m.signals[c.accs].rows();
             x.ds = m.signals[c.src].rows();
             x.src_feed = -1;
+            x.src_xb = ens_of_xhat.count(c.src) ? fe[ens_of_xhat.at(c.src)].xb_row : -1;
+            if (c.dst_ens < 0) orphans.push_back(static_cast<int32_t>(fc.size()));
             if (slot_of_sig.count(c.src)) {
                 x.src_feed = slot_of_sig[c.src];
                 if (m.feed_slots[x.src_feed].dim != x.ds) fail("feed slot dim differs from its signal");
@@ -460,6 +465,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
                 pr.per_batch = per_batch(s);
                 pr.index = static_cast<int32_t>(q);
                 pr.feed_slot = slot_of_sig.count(s) ? slot_of_sig[s] : -1;
+                pr.xb_row = ens_of_xhat.count(s) ? fe[ens_of_xhat.at(s)].xb_row : -1;
                 if (pr.feed_slot >= 0 && m.feed_slots[pr.feed_slot].dim != pr.dim)
                     fail("feed slot dim differs from its signal");
                 fp.push_back(pr);
@@ -495,7 +501,11 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         };
         upload(impl->d_ens, fe.data(), fe.size() * sizeof(FEns));
         upload(impl->d_conns, fc.data(), fc.size() * sizeof(FConn));
-        upload(impl->d_incoming, incoming.data(), incoming.size() * sizeof(int64_t));
+        upload(impl->d_incoming, incoming.data(), incoming.size() * sizeof(int32_t));
+        upload(impl->d_orphans, orphans.data(), orphans.size() * sizeof(int32_t));
+        impl->d_xbuf.ensure(static_cast<size_t>(2) * std::max(xrows, 1) * B * sizeof(float));
+        cuda_check(cudaMemset(impl->d_xbuf.p, 0, static_cast<size_t>(2) * std::max(xrows, 1) * B * sizeof(float)),
+                   "xbuf clear");
         upload(impl->d_values, values.data(), values.size() * sizeof(float));
         upload(impl->d_probes, fp.data(), fp.size() * sizeof(FProbe));
         upload(impl->d_feeds, ff.data(), ff.size() * sizeof(FFeed));
@@ -503,7 +513,11 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         p.values = impl->d_values.as<float>();
         p.ens = impl->d_ens.as<FEns>();
         p.conns = impl->d_conns.as<FConn>();
-        p.incoming = impl->d_incoming.as<int64_t>();
+        p.incoming = impl->d_incoming.as<int32_t>();
+        p.orphans = impl->d_orphans.as<int32_t>();
+        p.xbuf = impl->d_xbuf.as<float>();
+        p.xrows = xrows;
+        p.n_orphans = static_cast<int32_t>(orphans.size());
         p.probes = impl->d_probes.as<FProbe>();
         p.feeds = impl->d_feeds.as<FFeed>();
         p.n_ens = static_cast<int32_t>(fe.size());
@@ -513,14 +527,24 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         p.batch = B;
         p.btiles = (B + 31) / 32;
         p.nmax = (nmax + 31) / 32 * 32;
-        p.nwords = (nmax + 31) / 32;
         p.pmax_floats = pmax_floats;
-        // stage the decoder products with the encoders when the CTA's shared
-        // memory stays small enough for three CTAs per SM
+        // tiles per unit (one warp each) and warps per tile (neuron slices)
         {
-            size_t base = 128 + static_cast<size_t>(p.nmax) * DMAX * 4 + static_cast<size_t>(p.nmax) * 8 +
-                          DMAX * 128 + static_cast<size_t>(p.nwords) * 128 + 1024 * 16 + 8 * 13 * 32 * 4;
-            p.stage_dec = base + static_cast<size_t>(pmax_floats) * 4 <= 72 * 1024 ? 1 : 0;
+            int tu = 1;
+            while (tu < 8 && tu < p.btiles) tu *= 2;
+            p.tu = tu;
+            p.slices = 8 / tu;
+            p.groups = (p.btiles + tu - 1) / tu;
+        }
+        // stage the decoder products with the encoders when shared memory
+        // allows; prefer a footprint with two CTAs per SM
+        {
+            constexpr size_t two = 113 * 1024, one = 227 * 1024;
+            p.stage_dec = 1;
+            const size_t with = fused_smem_bytes(p, DMAX);
+            p.stage_dec = 0;
+            const size_t without = fused_smem_bytes(p, DMAX);
+            p.stage_dec = (with <= two || (without > two && with <= one)) ? 1 : 0;
         }
         p.dt = dt;
         if (time_op >= 0) {
@@ -534,12 +558,13 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         impl->dmax = fused_dmax_for(dmax_need);
         int cap = fused_max_grid(p, impl->dmax, eng.device());
         if (cap <= 0) fail("fused kernel does not fit on the device");
-        int64_t work = std::max<int64_t>(static_cast<int64_t>(p.n_ens) * p.btiles,
+        int64_t work = std::max<int64_t>(static_cast<int64_t>(p.n_ens) * p.groups,
                                          (static_cast<int64_t>(p.n_conn) * B + 255) / 256);
         impl->grid = static_cast<int>(std::min<int64_t>(cap, std::max<int64_t>(1, work)));
         std::ostringstream os;
         os << "fused: " << p.n_ens << " ensembles, " << p.n_conn << " connections, dmax " << impl->dmax << ", grid "
-           << impl->grid;
+           << impl->grid << ", tiles/unit " << p.tu << ", slices " << p.slices << ", stage_dec " << p.stage_dec
+           << ", smem " << fused_smem_bytes(p, impl->dmax);
         impl->desc = os.str();
         return impl;
     } catch (const Fail& f) {

@@ -1,27 +1,32 @@
 // fused.cu — the fused ensemble pipeline: one persistent cooperative kernel
-// advancing K timesteps, two grid barriers per step (see fused.hpp).
+// advancing K timesteps with ONE grid barrier per step (see fused.hpp).
 //
-// Phase A unit = (ensemble, 32-column batch tile), claimed dynamically;
-// lane = batch column, warp = a contiguous range of neurons:
-//   * the ensemble's zero-padded encoder rows, biases and (when they fit)
-//     decoder products are staged into shared memory by TMA bulk copies
-//     (cp.async.bulk + mbarrier) issued at unit start, overlapping the input sums;
-//   * the input vector of each column lives in DMAX registers for the unit;
-//   * v/r stream coalesced (arena layout [row][B]: 128 B per warp access) with
-//     evict-first hints and one round of software prefetch;
-//   * the two transcendental branches of the LIF step (expm1 for the step a
-//     neuron leaves its refractory period, log1p for the spike time) are
-//     evaluated inline from a double Taylor polynomial — the value glibc
-//     returns except on calibrated exceptions, all of which lie next to a
-//     float rounding midpoint.  A result in that window is used speculatively
-//     and its neuron is queued; after the sweep one parallel pass recomputes
-//     the queued neurons exactly (with table probes) and patches v, r and the
-//     spike bit.  No probe latency sits inside the sweep.
-//   * spikes leave the LIF as ballot words, are bit-transposed with ballots,
-//     and the decoder walks only set bits in ascending neuron order.
-// Zero padding (encoder rows to DMAX, transforms to DMAX) and skipping
-// non-spiking neurons are exact: a running sum that starts at +0 is never -0,
-// and x + (+-0) == x for every x, so the extra +0 terms change no bit.
+// Unit = (ensemble, group of tu 32-column batch tiles), claimed dynamically by
+// CTAs; each warp owns one tile (lane = batch column) and, when a unit has
+// fewer tiles than warps, a slice of the neurons.
+//   * encoders, biases and (when they fit) decoder spike products are staged
+//     into shared memory by bulk copies (cp.async.bulk + mbarrier) issued at
+//     unit start, overlapping the connection updates;
+//   * the connection updates of step k-1 run on the destination side, so the
+//     filter state is read and written once per step and the only cross-CTA
+//     data is xhat, double-buffered by step parity;
+//   * the neuron sweep streams v/r coalesced ([row][B] arena layout, 128 B per
+//     warp access, evict-first) and does the common LIF step inline; the two
+//     transcendental branches (log1p at a spike, expm1 on the step a neuron
+//     leaves its refractory period — each taken by ~25% of neuron-updates on
+//     the config-4 network) leave through warp-aggregated shared-memory queues
+//     (ballot + popc, no atomics) and are evaluated 32 at a time, one per lane,
+//     so their cost follows the spike rate instead of P(any lane of 32);
+//   * transcendentals use a double Taylor polynomial whose rounding is glibc's
+//     except inside a calibrated window next to float rounding midpoints; a
+//     doubtful value goes to a third queue that resolves it exactly (table
+//     probes) and patches v, r and the spike bit;
+//   * spikes are ballot words (bit = column); the decoder transposes 32x32 bit
+//     blocks with shuffles and walks each column's set bits in ascending neuron
+//     order, adding the precomputed products fp32(D[r,i]) * fp32(amp/dt).
+// Zero padding (encoder rows and transforms to DMAX) and skipping non-spiking
+// neurons are exact: a running sum that starts at +0 is never -0, and
+// x + (+-0) == x for every x, so the extra +0 terms change no bit.
 //
 // Every other floating-point operation is the reference's, in its order:
 //   in   : Reset payload, then += filtered_c for c in plan-group order (exec.cpp:189-210)
@@ -43,8 +48,11 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kUnroll = 4;
-constexpr int kFixCap = 1024;  // per-CTA fix-up entries (overflow is resolved inline, exactly)
+constexpr int kUnroll = 8;   // neuron rows per prefetch round (pairs inside)
+constexpr int kL2Ahead = 24; // rows of v/r pulled into L2 ahead of the round being computed
+constexpr uint32_t kFull = 0xffffffffu;
+// per-warp doubt queue capacity: <= 31 pending + 64 from a neuron pair
+constexpr int kQEntries = 96;
 
 __device__ __forceinline__ void grid_sync(cg::grid_group& g) {
     if (gridDim.x == 1)
@@ -53,7 +61,7 @@ __device__ __forceinline__ void grid_sync(cg::grid_group& g) {
         g.sync();
 }
 
-// ---- TMA bulk copy + mbarrier (sm_90+ async proxy) -------------------------
+// ---- bulk copy + mbarrier (sm_90+ async proxy) -------------------------
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -82,6 +90,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+/// Pull `bytes` (multiple of 16, 16-B aligned) of global memory into L2 (TMA prefetch).
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void prefetch_l2_line(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
 }
 
 // ---- optional section timers (PROF instantiation; thread 0 of each CTA) ----
@@ -117,42 +137,54 @@ struct Ticker {
     }
 };
 
-struct FixEntry {
-    int32_t key;  // neuron << 5 | lane
-    float v, r, J;
+struct __align__(16) QEnt {
+    uint32_t key;  // neuron << 5 | lane
+    float a, b, c; // the step's original v, r, J
 };
 
 struct Smem {
     uint64_t* bar;
+    int* cur;      // the CTA's current unit
     float* E;      // nmax x DMAX (zero padded)
     float* bias;   // nmax
     float* P;      // decoder products [n][dx] (when p.stage_dec)
-    float* in;     // DMAX x 32
-    uint32_t* words;
-    uint32_t* col;
-    FixEntry* fix;  // kFixCap
-    int* nfix;
-    int* next_unit;
+    float* in;     // tu x DMAX x 32
+    uint32_t* words;  // tu x nmax: spike ballot of neuron i in tile slot t (bit = lane)
+    QEnt* q;          // kWarps x kQEntries
+    float* ring;      // kWarps x [2 stages][v, r][kUnroll rows][32]
 };
 
-/// lif_spike_step<float> resolved exactly (table probes as needed); returns
-/// whether the neuron spiked.
-__device__ __forceinline__ bool lif_exact(float J, float& v, float& r, float dt, float tau_rc, float tau_ref,
-                                          const LibmTables& t) {
-    float delta = dt - r;
-    if (delta < 0.0f) delta = 0.0f;
-    if (delta > dt) delta = dt;
-    float vn = v - (J - v) * glibc_expm1f(-delta / tau_rc, t);
-    if (vn < 0.0f) vn = 0.0f;
-    if (vn > 1.0f) {
-        const float since = -tau_rc * glibc_log1pf(-(vn - 1.0f) / (J - 1.0f), t);
-        v = 0.0f;
-        r = tau_ref - since;
-        return true;
-    }
-    v = vn;
-    r = r > dt ? r - dt : 0.0f;
-    return false;
+constexpr int kRingFloats = 2 * 2 * kUnroll * 32;  // per warp
+
+template <int DMAX>
+__device__ Smem carve(uint32_t* base, const FusedProgram& p) {
+    Smem S;
+    char* at = reinterpret_cast<char*>(base);
+    S.bar = reinterpret_cast<uint64_t*>(at);
+    S.cur = reinterpret_cast<int*>(at + 8);
+    at += 128;
+    S.ring = reinterpret_cast<float*>(at);
+    at += static_cast<size_t>(kWarps) * kRingFloats * 4;
+    S.E = reinterpret_cast<float*>(at);
+    at += static_cast<size_t>(p.nmax) * DMAX * 4;
+    S.bias = reinterpret_cast<float*>(at);
+    at += static_cast<size_t>(p.nmax) * 4;
+    S.P = reinterpret_cast<float*>(at);
+    at += static_cast<size_t>(p.stage_dec ? p.pmax_floats : 0) * 4;
+    S.in = reinterpret_cast<float*>(at);
+    at += static_cast<size_t>(p.tu) * DMAX * 32 * 4;
+    S.words = reinterpret_cast<uint32_t*>(at);
+    at += static_cast<size_t>(p.tu) * p.nmax * 4;
+    S.q = reinterpret_cast<QEnt*>(at);
+    return S;
+}
+
+template <int DMAX>
+size_t smem_bytes(const FusedProgram& p) {
+    return 128 + static_cast<size_t>(kWarps) * kRingFloats * 4 + static_cast<size_t>(p.nmax) * DMAX * 4 +
+           static_cast<size_t>(p.nmax) * 4 + static_cast<size_t>(p.stage_dec ? p.pmax_floats : 0) * 4 +
+           static_cast<size_t>(p.tu) * DMAX * 32 * 4 + static_cast<size_t>(p.tu) * p.nmax * 4 +
+           sizeof(QEnt) * kQEntries * kWarps;
 }
 
 /// The batch width: BT when the kernel is specialised for it (row strides then
@@ -165,19 +197,228 @@ __device__ __forceinline__ int batch_of(const FusedProgram& p) {
         return p.batch;
 }
 
-template <int DMAX, int BT, bool PROF>
-__device__ void phase_a_unit(const FusedProgram& p, int unit, bool last, const Smem& S, uint32_t parity,
-                             Ticker<PROF>& tk) {
-    const int B = batch_of<BT>(p);
-    const int t = unit / p.btiles;
-    const int b0 = (unit - t * p.btiles) * 32;
-    const FEns& e = p.ens[t];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int b = b0 + lane;
-    const bool valid = (BT > 0 && BT % 32 == 0) || b < B;
-    float* A = p.arena;
+/// Warp-aggregated push: lanes with `pred` append `e` in lane order; returns the new count.
+__device__ __forceinline__ int qpush(QEnt* q, int n, bool pred, const QEnt& e) {
+    const uint32_t m = __ballot_sync(kFull, pred);
+    if (pred) q[n + __popc(m & lanemask_lt())] = e;
+    return n + __popc(m);
+}
 
-    // stage encoders, biases and decoder products (async; overlaps A1)
+// ---- async row copies (cp.async, LDGSTS) ------------------------------------
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+/// Copy rows [i, i + kUnroll) (those below n1) of v and r, columns [b0, b0 + 32)
+/// of this tile, into ring stage `st`.  vec: 16-B chunks (B % 4 == 0), else 4-B.
+__device__ __forceinline__ void ring_issue(float* ring, int st, const float* vrow0, const float* rrow0, int i, int n1,
+                                           int B, int b0, int lane, bool vec) {
+    float* dst = ring + st * (2 * kUnroll * 32);
+    if (vec) {
+        const int c4 = (lane & 7) * 4;
+        if (b0 + c4 < B) {
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                for (int h = 0; h < kUnroll / 4; ++h) {
+                    const int rr = 4 * h + (lane >> 3);
+                    if (i + rr < n1)
+                        cp_async16(dst + (a * kUnroll + rr) * 32 + c4,
+                                   (a ? rrow0 : vrow0) + static_cast<int64_t>(i + rr) * B + c4);
+                }
+        }
+    } else if (b0 + lane < B) {
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int rr = 0; rr < kUnroll; ++rr)
+                if (i + rr < n1)
+                    cp_async4(dst + (a * kUnroll + rr) * 32 + lane,
+                              (a ? rrow0 : vrow0) + static_cast<int64_t>(i + rr) * B + lane);
+    }
+    cp_async_commit();
+}
+
+/// lif_spike_step<float> resolved exactly (table probes as needed); returns
+/// whether the neuron spiked.
+__device__ __forceinline__ bool lif_exact(float J, float& v, float& r, float dt, float tau_rc, float tau_ref,
+                                          const LibmTables& t) {
+    float delta = dt - r;
+    if (delta < 0.0f) delta = 0.0f;
+    if (delta > dt) delta = dt;
+    float vn = v - (J - v) * glibc_spec_resolved(-delta / tau_rc, false, t);
+    if (vn < 0.0f) vn = 0.0f;
+    if (vn > 1.0f) {
+        const float since = -tau_rc * glibc_spec_resolved(-(vn - 1.0f) / (J - 1.0f), true, t);
+        v = 0.0f;
+        r = tau_ref - since;
+        return true;
+    }
+    v = vn;
+    r = r > dt ? r - dt : 0.0f;
+    return false;
+}
+
+/// Doubtful values (out of line: ~5% of transcendentals): lif_spike_step
+/// recomputed exactly from the original v, r, J; patches v, r and the spike
+/// bit.  Lane l takes entry l of q[0, cnt).
+__device__ __noinline__ void dq_batch(const QEnt* q, int cnt, const FEns* e, float* A, int B, int b0,
+                                      uint32_t* words, const LibmTables* lt, int lane) {
+    if (lane >= cnt) return;
+    const QEnt x = q[lane];
+    const uint32_t i = x.key >> 5, col = x.key & 31u;
+    const int64_t o = static_cast<int64_t>(i) * B + b0 + col;
+    float v = x.a, r = x.b;
+    if (lif_exact(x.c, v, r, e->dt, e->tau_rc, e->tau_ref, *lt))
+        atomicOr(words + i, 1u << col);
+    else
+        atomicAnd(words + i, ~(1u << col));
+    A[e->v_base + o] = v;
+    A[e->r_base + o] = r;
+}
+
+// ---- connections ----------------------------------------------------------
+
+/// Step-kk update of connection cn for batch column b, rows [r_lo, r_hi):
+/// acc = payload + T.src(kk) (sequential in j); f = a*state + b*acc; state = f.
+/// Returns f in f_out[r].  last: also write acc and filt to the arena.
+template <int DMAX, int BT>
+__device__ __forceinline__ void conn_rows(const FusedProgram& p, const FConn& cn, int kk, int b, int r_lo, int r_hi,
+                                          bool valid, bool last, float* f_out) {
+    const int B = batch_of<BT>(p);
+    float* A = p.arena;
+    const float* src;
+    if (cn.src_xb >= 0)
+        src = p.xbuf + (static_cast<int64_t>(kk & 1) * p.xrows + cn.src_xb) * B + b;
+    else if (cn.src_feed >= 0 && p.feed_present[cn.src_feed])
+        src = p.feed_data + p.feed_off[cn.src_feed] + static_cast<int64_t>(kk) * cn.ds * B + b;
+    else
+        src = A + cn.src_base + b;
+    float x[DMAX], s0[DMAX];
+#pragma unroll
+    for (int j = 0; j < DMAX; ++j) x[j] = (valid && j < cn.ds) ? src[static_cast<int64_t>(j) * B] : 0.0f;
+    float* st = A + cn.state_base + b;
+#pragma unroll
+    for (int r = 0; r < DMAX; ++r) s0[r] = (valid && r >= r_lo && r < r_hi) ? st[static_cast<int64_t>(r) * B] : 0.0f;
+    const float4* Tm = reinterpret_cast<const float4*>(p.values + cn.tpad_off);
+#pragma unroll
+    for (int r = 0; r < DMAX; ++r) {
+        if (r < r_lo || r >= r_hi) continue;
+        float acc = 0.0f;
+#pragma unroll
+        for (int q = 0; q < DMAX / 4; ++q) {
+            const float4 w = __ldg(Tm + r * (DMAX / 4) + q);
+            acc = acc + w.x * x[4 * q];
+            acc = acc + w.y * x[4 * q + 1];
+            acc = acc + w.z * x[4 * q + 2];
+            acc = acc + w.w * x[4 * q + 3];
+        }
+        const float accv = __ldg(p.values + cn.acc_init_off + r) + acc;
+        const float f = cn.a * s0[r] + cn.b * accv;  // lowpass_step (neuron_math.hpp:39-42)
+        f_out[r] = f;
+        if (valid) {
+            st[static_cast<int64_t>(r) * B] = f;
+            if (last) {
+                A[cn.acc_base + static_cast<int64_t>(r) * B + b] = accv;
+                A[cn.filt_base + static_cast<int64_t>(r) * B + b] = f;
+            }
+            if (cn.probe_filt >= 0)
+                p.ring[p.ring_off[cn.probe_filt] + (static_cast<int64_t>(kk) * cn.dd + r) * B + b] = f;
+            if (cn.probe_state >= 0)
+                p.ring[p.ring_off[cn.probe_state] + (static_cast<int64_t>(kk) * cn.dd + r) * B + b] = f;
+        }
+    }
+}
+
+/// Grid-stride work of step kk that is not owned by a unit: connection
+/// updates (all connections in the epilogue, destination-less ones otherwise),
+/// probe captures and the clock.
+template <int DMAX, int BT>
+__device__ void grid_step_work(const FusedProgram& p, int kk, bool all_conns, bool last) {
+    const int B = batch_of<BT>(p);
+    const int64_t gthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int nc = all_conns ? p.n_conn : p.n_orphans;
+    const int64_t items = static_cast<int64_t>(nc) * B;
+    for (int64_t it = gtid; it < items; it += gthreads) {
+        const int q = static_cast<int>(it / B);
+        const int b = static_cast<int>(it - static_cast<int64_t>(q) * B);
+        const int c = all_conns ? q : __ldg(p.orphans + q);
+        float f[DMAX];
+        conn_rows<DMAX, BT>(p, p.conns[c], kk, b, 0, p.conns[c].dd, true, last, f);
+    }
+    for (int q = 0; q < p.n_probes; ++q) {
+        const FProbe& pr = p.probes[q];
+        const int64_t n = static_cast<int64_t>(pr.dim) * B;
+        float* dst = p.ring + p.ring_off[pr.index] + static_cast<int64_t>(kk) * pr.dim * B;
+        const bool fed = pr.feed_slot >= 0 && p.feed_present[pr.feed_slot];
+        for (int64_t i = gtid; i < n; i += gthreads) {
+            const int64_t d = i / B;
+            const int bb = static_cast<int>(i - d * B);
+            float val;
+            if (pr.xb_row >= 0)
+                val = p.xbuf[(static_cast<int64_t>(kk & 1) * p.xrows + pr.xb_row + d) * B + bb];
+            else if (fed)
+                val = p.feed_data[p.feed_off[pr.feed_slot] + static_cast<int64_t>(kk) * pr.dim * B + d * B +
+                                  (pr.per_batch ? bb : 0)];
+            else
+                val = p.arena[pr.base + (pr.per_batch ? d * B + bb : d)];
+            dst[i] = val;
+        }
+    }
+    if (p.has_time && gtid == 0) {  // TimeUpdate (exec.cpp:300-309)
+        const float next = p.arena[p.step_base] + 1.0f;
+        p.arena[p.step_base] = next;
+        p.arena[p.time_base] = next * p.dt;
+        if (p.time_probe_step >= 0)
+            for (int bb = 0; bb < B; ++bb) p.ring[p.ring_off[p.time_probe_step] + static_cast<int64_t>(kk) * B + bb] = next;
+        if (p.time_probe_time >= 0)
+            for (int bb = 0; bb < B; ++bb)
+                p.ring[p.ring_off[p.time_probe_time] + static_cast<int64_t>(kk) * B + bb] = next * p.dt;
+    }
+}
+
+// ---- bit transpose --------------------------------------------------------
+
+/// Lane r holds row r of a 32x32 bit matrix (bit c = M[r][c]); returns column
+/// `lane` (bit r = M[r][lane]).  Recursive block swap, five shuffle rounds.
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+    constexpr uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+        const int j = 16 >> s;
+        const uint32_t m = masks[s];
+        const uint32_t y = __shfl_xor_sync(kFull, x, j);
+        x = (lane & j) ? ((x & ~m) | ((y >> j) & m)) : ((x & m) | ((y << j) & ~m));
+    }
+    return x;
+}
+
+// ---- the unit ---------------------------------------------------------------
+
+template <int DMAX, int BT, bool PROF>
+__device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bool last, const Smem& S,
+                         uint32_t parity, Ticker<PROF>& tk) {
+    const int B = batch_of<BT>(p);
+    const int ei = u / p.groups;
+    const int g = u - ei * p.groups;
+    const FEns e = p.ens[ei];  // a private copy: fields stay in registers across the arena stores
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tslot = warp / p.slices, slice = warp - tslot * p.slices;
+    const int tile = g * p.tu + tslot;
+    const int b0 = tile * 32;
+    const bool active = tslot < p.tu && b0 < B;  // warp-uniform
+    const int b = b0 + lane;
+    const bool valid = active && ((BT > 0 && BT % 32 == 0) || b < B);
+    float* A = p.arena;
+    const LibmTables& lt = p.libm;
+
+    // stage encoders, biases and decoder products (async; overlaps the connection updates)
     if (threadIdx.x == 0) {
         fence_proxy_async_smem();  // prior generic accesses of the staging buffers are ordered first
         const uint32_t eb = static_cast<uint32_t>((e.n + 1) & ~1) * DMAX * 4, bb = static_cast<uint32_t>(e.n_pad) * 4;
@@ -186,76 +427,103 @@ __device__ void phase_a_unit(const FusedProgram& p, int unit, bool last, const S
         bulk_g2s(S.E, p.values + e.epad_off, eb, S.bar);
         bulk_g2s(S.bias, p.values + e.bias_off, bb, S.bar);
         if (pb) bulk_g2s(S.P, p.values + e.dec_scaled_off, pb, S.bar);
-        *S.nfix = 0;
     }
 
-    // A1: in[j] = payload[j] (+ filtered_c[j] for each incoming c, in plan order)
-    for (int idx = threadIdx.x; idx < DMAX * 32; idx += kThreads) {
-        const int j = idx >> 5;
-        float acc = 0.0f;
-        if (j < e.d) {
-            acc = __ldg(p.values + e.in_init_off + j);
-            if (valid) {
-                const float* col = A + static_cast<int64_t>(j) * B + b;
-                const int64_t* src = p.incoming + e.inc_begin;
-                int q = 0;
-                for (; q + 4 <= e.inc_count; q += 4) {  // four loads in flight, summed in order
-                    const float f0 = col[__ldg(src + q)], f1 = col[__ldg(src + q + 1)];
-                    const float f2 = col[__ldg(src + q + 2)], f3 = col[__ldg(src + q + 3)];
-                    acc = acc + f0;
-                    acc = acc + f1;
-                    acc = acc + f2;
-                    acc = acc + f3;
-                }
-                for (; q < e.inc_count; ++q) acc = acc + col[__ldg(src + q)];
-                if (last) A[e.in_base + static_cast<int64_t>(j) * B + b] = acc;
+    // 1. connection updates of step k-1 (destination side) and the input sum, plan order
+    float* sin = S.in + tslot * DMAX * 32;
+    if (active) {
+        const int rper = (e.d + p.slices - 1) / p.slices;
+        const int r_lo = slice * rper, r_hi = min(e.d, r_lo + rper);
+        float in[DMAX];
+#pragma unroll
+        for (int r = 0; r < DMAX; ++r) in[r] = (r >= r_lo && r < r_hi) ? __ldg(p.values + e.in_init_off + r) : 0.0f;
+        for (int q = 0; q < e.inc_count; ++q) {
+            const FConn& cn = p.conns[__ldg(p.incoming + e.inc_begin + q)];
+            float f[DMAX];
+            if (do_update) {
+                conn_rows<DMAX, BT>(p, cn, k - 1, b, r_lo, r_hi, valid, false, f);
+            } else {
+#pragma unroll
+                for (int r = 0; r < DMAX; ++r)
+                    f[r] = (valid && r >= r_lo && r < r_hi) ? A[cn.state_base + static_cast<int64_t>(r) * B + b] : 0.0f;
+            }
+#pragma unroll
+            for (int r = 0; r < DMAX; ++r)
+                if (r >= r_lo && r < r_hi) in[r] = in[r] + f[r];
+        }
+#pragma unroll
+        for (int r = 0; r < DMAX; ++r) {
+            if (r >= r_lo && r < r_hi) {
+                sin[r * 32 + lane] = in[r];
+                if (last && valid) A[e.in_base + static_cast<int64_t>(r) * B + b] = in[r];
+            } else if (slice == 0 && r >= e.d) {
+                sin[r * 32 + lane] = 0.0f;  // padding rows hold +0
             }
         }
-        S.in[j * 32 + lane] = acc;  // padding rows hold +0
     }
-    __syncthreads();
+    if (p.slices > 1)
+        __syncthreads();
+    else
+        __syncwarp();
+    tk.tick(FS_IN);
 
     float x[DMAX];
 #pragma unroll
-    for (int j = 0; j < DMAX; ++j) x[j] = S.in[j * 32 + lane];
+    for (int j = 0; j < DMAX; ++j) x[j] = active ? sin[j * 32 + lane] : 0.0f;
     mbar_wait(S.bar, parity);
-    tk.tick(FS_A1);
 
-    // A2: encoder + lif_spike_step<float> (neuron_math.hpp:55-77), speculative transcendentals.
-    // Neurons go in pairs through the paired fp32 pipe (FADD2/FMUL2: two IEEE
-    // round-to-nearest operations per instruction, bit-identical to scalar ones);
-    // the rarely taken transcendental branches stay scalar.
-    const float dt = e.dt, tau_rc = e.tau_rc, tau_ref = e.tau_ref, amp_dt = e.amp_dt, em_dt = e.em_dt;
-    const int npw = ((e.n + kWarps - 1) / kWarps + kUnroll - 1) / kUnroll * kUnroll;
-    const int nbeg = warp * npw, nend = min(e.n, nbeg + npw);
-    float* vp = A + e.v_base + b + static_cast<int64_t>(nbeg) * B;  // row i0 of the current round
-    float* rp = A + e.r_base + b + static_cast<int64_t>(nbeg) * B;
-    const float2 dt2 = make_float2(dt, dt), ndt2 = make_float2(-dt, -dt);
-    float vnx[kUnroll], rnx[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-        vnx[u] = rnx[u] = 0.f;
-        if (nbeg + u < nend && valid) {
-            vnx[u] = __ldcs(vp + u * B);
-            rnx[u] = __ldcs(rp + u * B);
-        }
-    }
-    for (int i0 = nbeg; i0 < nend; i0 += kUnroll, vp += kUnroll * B, rp += kUnroll * B) {
-        float v[kUnroll], r[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            v[u] = vnx[u];
-            r[u] = rnx[u];
-            vnx[u] = rnx[u] = 0.f;
-            if (i0 + kUnroll + u < nend && valid) {  // prefetch the next round
-                vnx[u] = __ldcs(vp + (kUnroll + u) * B);
-                rnx[u] = __ldcs(rp + (kUnroll + u) * B);
+    // 2. neuron sweep over this warp's slice
+    const int nper = ((e.n + p.slices - 1) / p.slices + 31) & ~31;
+    const int n0 = min(e.n, slice * nper), n1 = min(e.n, n0 + nper);
+    uint32_t* words = S.words + tslot * p.nmax;
+    if (active && n0 < n1) {
+        QEnt* dq = S.q + warp * kQEntries;
+        int dn = 0;
+        const float dt = e.dt, em_dt = e.em_dt, tau_rc = e.tau_rc, tau_ref = e.tau_ref;
+        const double inv_tau_rc = e.inv_tau_rc;
+        const float2 dt2 = make_float2(dt, dt), ndt2 = make_float2(-dt, -dt);
+        float* vrow0 = A + e.v_base + b0;  // row 0, column b0 of this tile
+        float* rrow0 = A + e.r_base + b0;
+        float* ring = S.ring + warp * kRingFloats;
+        const bool vec = (B & 3) == 0;
+        // L2 prefetch kL2Ahead rows ahead.  When the unit spans every column the
+        // rows are contiguous: lane 0 of the slice's first tile pulls 8 whole rows
+        // of v and of r with two bulk prefetches; otherwise lanes 0-15 pull their
+        // tile's 128-B segments of the 8 v and 8 r rows.
+        const bool pf_rows = p.groups == 1 && p.tu * 32 >= B && vec;
+        const bool pf_lane = pf_rows ? (tslot == 0 && lane == 0) : lane < 2 * kUnroll;
+        const float* pf_v = A + e.v_base + (pf_rows ? 0 : b0 + (lane & (kUnroll - 1)) * static_cast<int64_t>(B));
+        const float* pf_r = A + e.r_base + (pf_rows ? 0 : b0 + (lane & (kUnroll - 1)) * static_cast<int64_t>(B));
+        const float* pf_base = (pf_rows || lane < kUnroll) ? pf_v : pf_r;
+        float* vst = vrow0 + static_cast<int64_t>(n0) * B + lane;  // row i of this lane
+        const int64_t rdelta = e.r_base - e.v_base;
+        ring_issue(ring, 0, vrow0, rrow0, n0, n1, B, b0, lane, vec);
+        for (int i = n0; i < n1; i += 2, vst += 2 * B) {
+            const int rel = i - n0;
+            const int st = (rel >> 3) & 1, rr = rel & (kUnroll - 1);
+            if (rr == 0) {
+                __syncwarp();  // every lane's reads of the stage being refilled are done
+                ring_issue(ring, st ^ 1, vrow0, rrow0, i + kUnroll, n1, B, b0, lane, vec);
+                cp_async_wait1();
+                __syncwarp();
+                const int pi = i + kL2Ahead;
+                if (pf_lane && pi < n1) {
+                    if (pf_rows) {
+                        const uint32_t nb = static_cast<uint32_t>(min(kUnroll, n1 - pi) * B) * 4u;
+                        prefetch_l2_bulk(pf_v + static_cast<int64_t>(pi) * B, nb);
+                        prefetch_l2_bulk(pf_r + static_cast<int64_t>(pi) * B, nb);
+                    } else if (pi + (lane & (kUnroll - 1)) < n1) {
+                        const float* pa = pf_base + static_cast<int64_t>(pi) * B;
+                        if (vec)
+                            prefetch_l2_bulk(pa, static_cast<uint32_t>(min(32, B - b0)) * 4u);
+                        else
+                            prefetch_l2_line(pa);
+                    }
+                }
             }
-        }
-#pragma unroll
-        for (int k = 0; k < kUnroll / 2; ++k) {
-            const int i = i0 + 2 * k;
-            if (i >= nend) break;  // warp-uniform
+            const float* sv = ring + st * (2 * kUnroll * 32) + rr * 32 + lane;
+            const float2 v2 = make_float2(sv[0], sv[32]);
+            const float2 r2 = make_float2(sv[kUnroll * 32], sv[kUnroll * 32 + 32]);
             // DotInc(E, in, J) for neurons i, i+1: acc from +0, j ascending, then J = bias + acc.
             // Products two dims at a time (FMUL2), sums scalar and in order.  A
             // paired product must never feed a paired sum: ptxas contracts
@@ -278,303 +546,168 @@ __device__ void phase_a_unit(const FusedProgram& p, int unit, bool last, const S
                 acc[h] = a;
             }
             const float2 J2 = __fadd2_rn(*reinterpret_cast<const float2*>(S.bias + i), make_float2(acc[0], acc[1]));
-            const float2 v2 = make_float2(v[2 * k], v[2 * k + 1]), r2 = make_float2(r[2 * k], r[2 * k + 1]);
             const float2 dl2 = __fadd2_rn(dt2, make_float2(-r2.x, -r2.y));  // dt - r
             const float2 rr2 = __fadd2_rn(r2, ndt2);                        // r - dt
+            // lif_spike_step<float> (neuron_math.hpp:55-77) with both transcendentals
+            // evaluated speculatively on every lane (at ~25% spikes and ~25% refractory
+            // exits per step nearly every warp row needs both): a double polynomial,
+            // rounded, exact unless `doubtful`; doubtful or out-of-range lanes are
+            // recomputed exactly in the doubt queue from their original v, r, J.
             float em[2];
-            bool doubt[2];
+            bool ex[2], dbt[2];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                float delta = h ? dl2.y : dl2.x;
-                if (delta < 0.0f) delta = 0.0f;
-                if (delta > dt) delta = dt;
-                // expm1(-delta/tau_rc): delta == dt -> the host glibc value; delta == +0 -> expm1(-0) = -0
-                em[h] = delta == dt ? em_dt : -0.0f;
-                doubt[h] = false;
-                if (valid && delta != dt && delta != 0.0f) {
-                    // == -delta / tau_rc in IEEE float: the double product is within 2^-52 of the quotient,
-                    // and a quotient of floats is never within 2^-49 of a float midpoint unless on it,
-                    // which needs a power-of-two divisor (then the product is exact)
-                    const float xa = static_cast<float>(static_cast<double>(-delta) * e.inv_tau_rc);
-                    if (lif_range(xa)) {
-                        const Spec s = spec_lif(xa, false, p.libm);
-                        em[h] = s.r;
-                        doubt[h] = s.doubtful;
-                    } else {
-                        em[h] = glibc_expm1f(xa, p.libm);
-                    }
-                }
+                const float delta = h ? dl2.y : dl2.x;  // clamp to [0, dt] below, NaN kept
+                const bool ge = delta >= dt, le = delta <= 0.0f;
+                ex[h] = !ge && !le;  // 0 < delta < dt (or NaN): the step leaving the refractory period
+                // == -delta / tau_rc in IEEE float: the double product is within 2^-52 of the quotient,
+                // and a quotient of floats is never within 2^-49 of a float midpoint unless on it,
+                // which needs a power-of-two divisor (then the product is exact)
+                const float xa = static_cast<float>(static_cast<double>(-delta) * inv_tau_rc);
+                const bool in_a = ex[h] && lif_range(xa);
+                const Spec sa = spec_expm1(in_a ? xa : -0.025f, lt);
+                em[h] = ex[h] ? sa.r : (ge ? em_dt : -0.0f);  // expm1(-dt/tau_rc) from the host; expm1(-0) = -0
+                dbt[h] = ex[h] && (!in_a || sa.doubtful);
             }
             // v - (J - v) * em: scalar products between the paired sums (see above)
             const float2 d2 = __fadd2_rn(J2, make_float2(-v2.x, -v2.y));
             const float t0 = __fmul_rn(d2.x, em[0]), t1 = __fmul_rn(d2.y, em[1]);
             const float2 vn2 = __fadd2_rn(v2, make_float2(-t0, -t1));
+            const bool two = i + 1 < n1;  // warp-uniform
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                if (h && i + 1 >= nend) break;  // warp-uniform
+                const bool row = h == 0 || two;
                 const float J = h ? J2.y : J2.x, vh = h ? v2.y : v2.x, rh = h ? r2.y : r2.x;
                 float vn = h ? vn2.y : vn2.x;
                 if (vn < 0.0f) vn = 0.0f;
-                const bool spike = valid && vn > 1.0f;
-                bool dbt = doubt[h];
-                float vo, ro;
-                if (spike) {
-                    const float xl = -(vn - 1.0f) / (J - 1.0f);
-                    float lg;
-                    if (lif_range(xl)) {
-                        const Spec s = spec_lif(xl, true, p.libm);
-                        lg = s.r;
-                        dbt = dbt || s.doubtful;
-                    } else {
-                        lg = glibc_log1pf(xl, p.libm);
-                    }
-                    const float since = -tau_rc * lg;
-                    vo = 0.0f;
-                    ro = tau_ref - since;
-                } else {
-                    vo = vn;
-                    ro = rh > dt ? (h ? rr2.y : rr2.x) : 0.0f;
+                const bool spike = vn > 1.0f;
+                const float xl = -(vn - 1.0f) / (J - 1.0f);
+                const bool in_l = spike && lif_range(xl);
+                const Spec sl = spec_log1p(in_l ? xl : -0.01f, lt);
+                const bool d = row && valid && (dbt[h] || (spike && (!in_l || sl.doubtful)));
+                const float since = -tau_rc * sl.r;
+                const float rn = spike ? tau_ref - since : (rh > dt ? (h ? rr2.y : rr2.x) : 0.0f);
+                if (row && valid && !d) {
+                    __stcs(vst + h * B, spike ? 0.0f : vn);
+                    __stcs(vst + h * B + rdelta, rn);
                 }
-                bool spike_final = spike;
-                if (dbt) {  // queue the neuron for exact resolution from its original inputs
-                    const int slot = atomicAdd(S.nfix, 1);
-                    if (slot < kFixCap) {
-                        S.fix[slot] = {((i + h) << 5) | lane, vh, rh, J};
-                    } else {  // queue full: resolve right here
-                        float ve = vh, re = rh;
-                        spike_final = lif_exact(J, ve, re, dt, tau_rc, tau_ref, p.libm);
-                        vo = ve;
-                        ro = re;
+                const uint32_t word = __ballot_sync(kFull, row && valid && spike);
+                if (row && lane == 0) words[i + h] = word;
+                const uint32_t dm = __ballot_sync(kFull, d);
+                if (dm) {  // warp-uniform
+                    if (d) dq[dn + __popc(dm & lanemask_lt())] = QEnt{(static_cast<uint32_t>(i + h) << 5) | lane, vh, rh, J};
+                    dn += __popc(dm);
+                }
+            }
+            if (dn >= 32) {
+                dn -= 32;
+                __syncwarp();
+                if constexpr (PROF) {
+                    if (lane == 0) {
+                        atomicAdd(p.prof + FS_COUNT + 2, 1ull);
+                        atomicAdd(p.prof + FS_COUNT + 3, 32ull);
                     }
                 }
-                const uint32_t word = __ballot_sync(0xffffffffu, spike_final);
-                if (valid) {
-                    __stcs(vp + (2 * k + h) * B, vo);
-                    __stcs(rp + (2 * k + h) * B, ro);
-                    if (last) {
-                        A[e.j_base + static_cast<int64_t>(i + h) * B + b] = J;
-                        A[e.out_base + static_cast<int64_t>(i + h) * B + b] = spike_final ? amp_dt : 0.0f;
-                    }
+                dq_batch(dq + dn, 32, p.ens + ei, A, B, b0, words, &p.libm, lane);
+                __syncwarp();
+            }
+        }
+        if (dn > 0) {
+            __syncwarp();
+            if constexpr (PROF) {
+                if (lane == 0) {
+                    atomicAdd(p.prof + FS_COUNT + 2, 1ull);
+                    atomicAdd(p.prof + FS_COUNT + 3, static_cast<unsigned long long>(dn));
                 }
-                if (lane == 0) S.words[i + h] = word;
+            }
+            dq_batch(dq, dn, p.ens + ei, A, B, b0, words, &p.libm, lane);
+            __syncwarp();
+        }
+        // the call's last step leaves J in the arena (DotInc(E, in, J) as above, once)
+        if (last && valid) {
+            for (int i = n0; i < n1; ++i) {
+                const float4* er = reinterpret_cast<const float4*>(S.E + i * DMAX);
+                float a = 0.0f;
+#pragma unroll
+                for (int q = 0; q < DMAX / 4; ++q) {
+                    const float4 w = er[q];
+                    a = a + w.x * x[4 * q];
+                    a = a + w.y * x[4 * q + 1];
+                    a = a + w.z * x[4 * q + 2];
+                    a = a + w.w * x[4 * q + 3];
+                }
+                A[e.j_base + static_cast<int64_t>(i) * B + b] = S.bias[i] + a;
             }
         }
     }
-    __syncthreads();
-    tk.tick(FS_A2);
+    tk.tick(FS_SWEEP);
+    if (p.slices > 1)
+        __syncthreads();
+    else
+        __syncwarp();
 
-    // A2': exact resolution of the queued neurons (all threads, probes overlap)
-    const int nfix = min(*S.nfix, kFixCap);
-    // Stage 1 re-derives the speculative arguments and probes the tables for
-    // both at once; only a real glibc exception (~0.6% of queued neurons)
-    // triggers the exact recomputation and the patch.
-    for (int f = threadIdx.x; f < nfix; f += kThreads) {
-        const FixEntry fe = S.fix[f];
-        const int i = fe.key >> 5, l = fe.key & 31;
-        float delta = dt - fe.r;
-        if (delta < 0.0f) delta = 0.0f;
-        if (delta > dt) delta = dt;
-        const float xe = -delta / tau_rc;
-        const bool pe = delta != dt && delta != 0.0f && lif_range(xe);
-        float em = delta == dt ? em_dt : -0.0f;
-        bool de = false;
-        if (delta != dt && delta != 0.0f) {
-            if (pe) {
-                const Spec s = spec_lif(xe, false, p.libm);
-                em = s.r;
-                de = s.doubtful;
-            } else {
-                em = glibc_expm1f(xe, p.libm);
-            }
-        }
-        float vn = fe.v - (fe.J - fe.v) * em;
-        if (vn < 0.0f) vn = 0.0f;
-        const float xl = -(vn - 1.0f) / (fe.J - 1.0f);
-        const bool dl = vn > 1.0f && lif_range(xl) && spec_lif(xl, true, p.libm).doubtful;
-        const LibmHash &h0 = p.libm.t[0], &h1 = p.libm.t[1];
-        const uint32_t ke = __float_as_uint(xe), kl = __float_as_uint(xl);
-        uint32_t ie = (ke * 0x9E3779B1u) >> h0.hot_shift, il = (kl * 0x9E3779B1u) >> h1.hot_shift;
-        unsigned long long se = de ? __ldg(h0.hot_slots + ie) : 0ull;  // both first probes in flight
-        unsigned long long sl = dl ? __ldg(h1.hot_slots + il) : 0ull;
-        while (se != 0ull && static_cast<uint32_t>(se >> 32) != ke) {
-            ie = (ie + 1u) & h0.hot_mask;
-            se = __ldg(h0.hot_slots + ie);
-        }
-        while (sl != 0ull && static_cast<uint32_t>(sl >> 32) != kl) {
-            il = (il + 1u) & h1.hot_mask;
-            sl = __ldg(h1.hot_slots + il);
-        }
-        if (se == 0ull && sl == 0ull) continue;  // neither value is an exception: the speculation stands
-        float ve = fe.v, re = fe.r;
-        const bool spk = lif_exact(fe.J, ve, re, dt, tau_rc, tau_ref, p.libm);
-        const int64_t o = static_cast<int64_t>(i) * B + b0 + l;
-        A[e.v_base + o] = ve;
-        A[e.r_base + o] = re;
-        if (last) A[e.out_base + o] = spk ? amp_dt : 0.0f;
-        if (spk != static_cast<bool>((S.words[i] >> l) & 1u)) atomicXor(S.words + i, 1u << l);
-    }
-    __syncthreads();
-    tk.tick(FS_FIX);
-
-    // A3: transpose neuron words (bit = column) into column words (bit = neuron)
-    const int nw = (e.n + 31) >> 5;
-    for (int w = warp; w < nw; w += kWarps) {
-        const int i = w * 32 + lane;
-        const uint32_t mine = i < e.n ? S.words[i] : 0u;
-#pragma unroll 8
-        for (int c = 0; c < 32; ++c) {
-            const uint32_t bits = __ballot_sync(0xffffffffu, (mine >> c) & 1u);
-            if (lane == c) S.col[c * p.nwords + w] = bits;
-        }
-    }
-    __syncthreads();
-    tk.tick(FS_A3);
-
-    // A4: decoders over the spiking neurons of each column, ascending i; the
-    // terms are the precomputed products fp32(D[r,i]) * fp32(amp/dt), stored
-    // transposed ([n][dx]).  Staged and dx % 4 == 0: lane = column, one warp
-    // per 4 decoded rows, one LDS.128 and four independent sums per spike.
-    if (p.stage_dec && (e.dx & 3) == 0) {
-        const int stride4 = e.dx >> 2;
-        const uint32_t* cw = S.col + lane * p.nwords;
-        for (int g = warp; g < stride4; g += kWarps) {
-            const float4* P4 = reinterpret_cast<const float4*>(S.P) + g;
-            float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+    // 3. decode: rows [r0, r0 + R) of this warp's tile over all neurons, ascending
+    if (active) {
+        const int dx = e.dx;
+        int R = (dx + p.slices - 1) / p.slices;
+        if ((dx & 3) == 0) R = (R + 3) & ~3;
+        const int r0 = slice * R;
+        if (r0 < dx) {
+            const int rn = min(R, dx - r0);
+            const float* Pb = (p.stage_dec ? S.P : p.values + e.dec_scaled_off) + r0;
+            const bool vec = (dx & 3) == 0 && (rn & 3) == 0;
+            float a[DMAX];
+#pragma unroll
+            for (int q = 0; q < DMAX; ++q) a[q] = 0.0f;
+            const int nw = (e.n + 31) >> 5;
             for (int w = 0; w < nw; ++w) {
-                uint32_t bits = cw[w];
+                const int i = w * 32 + lane;
+                uint32_t bits = transpose32(i < e.n ? words[i] : 0u, lane);
+                if (!valid) bits = 0u;
                 while (bits) {
-                    const int i1 = w * 32 + __ffs(bits) - 1;
+                    const int c = __ffs(bits) - 1;
                     bits &= bits - 1u;
-                    const float4 t = P4[i1 * stride4];
-                    a0 = a0 + t.x;
-                    a1 = a1 + t.y;
-                    a2 = a2 + t.z;
-                    a3 = a3 + t.w;
+                    const float* pr = Pb + static_cast<int64_t>(w * 32 + c) * dx;
+                    if (vec) {
+#pragma unroll
+                        for (int q = 0; q < DMAX / 4; ++q) {
+                            if (4 * q < rn) {
+                                const float4 t4 = *reinterpret_cast<const float4*>(pr + 4 * q);
+                                a[4 * q] = a[4 * q] + t4.x;
+                                a[4 * q + 1] = a[4 * q + 1] + t4.y;
+                                a[4 * q + 2] = a[4 * q + 2] + t4.z;
+                                a[4 * q + 3] = a[4 * q + 3] + t4.w;
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < DMAX; ++q)
+                            if (q < rn) a[q] = a[q] + pr[q];
+                    }
                 }
             }
             if (valid) {
-                const float* init = p.values + e.xhat_init_off + 4 * g;
-                float* xo = A + e.xhat_base + static_cast<int64_t>(4 * g) * B + b;
-                xo[0] = __ldg(init) + a0;
-                xo[B] = __ldg(init + 1) + a1;
-                xo[2 * B] = __ldg(init + 2) + a2;
-                xo[3 * B] = __ldg(init + 3) + a3;
-            }
-        }
-        __syncthreads();
-        tk.tick(FS_A4);
-        return;
-    }
-    // general layout: lanes are (column, row) with the row fastest, so the
-    // rows of one column walk the same spike list together
-    const int rd = e.dx <= 1 ? 1 : 1 << (32 - __clz(e.dx - 1));  // rows per column group (pow2 <= 32)
-    for (int idx = threadIdx.x; idx < 32 * rd; idx += kThreads) {
-        const int l = idx / rd, rrow = idx - l * rd, bb = b0 + l;
-        const bool act = bb < B && rrow < e.dx;
-        const float* pc = (p.stage_dec ? S.P : p.values + e.dec_scaled_off) + rrow;
-        float acc = 0.0f;
-        const uint32_t* cw = S.col + l * p.nwords;
-        for (int w = 0; w < nw; ++w) {
-            uint32_t bits = cw[w];
-            const float* pw = pc + static_cast<int64_t>(w) * 32 * e.dx;
-            while (bits) {
-                const int i1 = __ffs(bits) - 1;
-                bits &= bits - 1u;
-                if (bits) {
-                    const int i2 = __ffs(bits) - 1;
-                    bits &= bits - 1u;
-                    const float t1 = act ? pw[i1 * e.dx] : 0.f, t2 = act ? pw[i2 * e.dx] : 0.f;
-                    acc = acc + t1;
-                    acc = acc + t2;
-                } else {
-                    acc = acc + (act ? pw[i1 * e.dx] : 0.f);
+                float* xo = p.xbuf + (static_cast<int64_t>(k & 1) * p.xrows + e.xb_row + r0) * B + b;
+#pragma unroll
+                for (int q = 0; q < DMAX; ++q) {
+                    if (q < rn) {
+                        const float xv = __ldg(p.values + e.xhat_init_off + r0 + q) + a[q];
+                        xo[static_cast<int64_t>(q) * B] = xv;
+                        if (last) A[e.xhat_base + static_cast<int64_t>(r0 + q) * B + b] = xv;
+                    }
                 }
             }
         }
-        if (act) A[e.xhat_base + static_cast<int64_t>(rrow) * B + bb] = __ldg(p.values + e.xhat_init_off + rrow) + acc;
+        // out = amp/dt on a spike (the call's last step only reaches the arena)
+        if (last && valid)
+            for (int i = n0; i < n1; ++i)
+                A[e.out_base + static_cast<int64_t>(i) * B + b] = (words[i] >> lane) & 1u ? e.amp_dt : 0.0f;
     }
-    __syncthreads();
-    tk.tick(FS_A4);
-}
-
-template <int DMAX, int BT>
-__device__ __forceinline__ void phase_b_item(const FusedProgram& p, int c, int b, bool last, int ks) {
-    const int B = batch_of<BT>(p);
-    const FConn& cn = p.conns[c];
-    float* A = p.arena;
-    float x[DMAX];
-    // a fed source is read straight from the staged feed block of step ks
-    // (write_feeds precedes every reader, exec.cpp:353-356); the arena copy
-    // of fed nodes is refreshed on a call's last step only
-    const float* src = (cn.src_feed >= 0 && p.feed_present[cn.src_feed])
-                           ? p.feed_data + p.feed_off[cn.src_feed] + static_cast<int64_t>(ks) * cn.ds * B + b
-                           : A + cn.src_base + b;
-#pragma unroll
-    for (int j = 0; j < DMAX; ++j) x[j] = j < cn.ds ? src[j * B] : 0.0f;
-    const float4* T = reinterpret_cast<const float4*>(p.values + cn.tpad_off);
-    float* st = A + cn.state_base + b;
-    float s0[DMAX];  // every state load in flight before the arithmetic
-#pragma unroll
-    for (int r = 0; r < DMAX; ++r) s0[r] = r < cn.dd ? st[r * B] : 0.0f;
-#pragma unroll
-    for (int r = 0; r < DMAX; ++r) {
-        if (r >= cn.dd) break;
-        float acc = 0.0f;
-#pragma unroll
-        for (int q = 0; q < DMAX / 4; ++q) {
-            const float4 w = __ldg(T + r * (DMAX / 4) + q);
-            acc = acc + w.x * x[4 * q];
-            acc = acc + w.y * x[4 * q + 1];
-            acc = acc + w.z * x[4 * q + 2];
-            acc = acc + w.w * x[4 * q + 3];
-        }
-        const float accv = __ldg(p.values + cn.acc_init_off + r) + acc;
-        const float f = cn.a * s0[r] + cn.b * accv;  // lowpass_step (neuron_math.hpp:39-42)
-        st[r * B] = f;
-        if (last) {
-            A[cn.acc_base + static_cast<int64_t>(r) * B + b] = accv;
-            A[cn.filt_base + static_cast<int64_t>(r) * B + b] = f;
-        }
-        if (cn.probe_filt >= 0)
-            p.ring[p.ring_off[cn.probe_filt] + (static_cast<int64_t>(ks) * cn.dd + r) * B + b] = f;
-        if (cn.probe_state >= 0)
-            p.ring[p.ring_off[cn.probe_state] + (static_cast<int64_t>(ks) * cn.dd + r) * B + b] = f;
-    }
-}
-
-template <int DMAX>
-__device__ Smem carve(uint32_t* base, const FusedProgram& p) {
-    Smem S;
-    char* at = reinterpret_cast<char*>(base);
-    S.bar = reinterpret_cast<uint64_t*>(at);
-    S.nfix = reinterpret_cast<int*>(at + 8);
-    S.next_unit = reinterpret_cast<int*>(at + 12);
-    at += 128;
-    S.E = reinterpret_cast<float*>(at);
-    at += static_cast<size_t>(p.nmax) * DMAX * 4;
-    S.bias = reinterpret_cast<float*>(at);
-    at += static_cast<size_t>(p.nmax) * 4;
-    S.P = reinterpret_cast<float*>(at);
-    at += static_cast<size_t>(p.stage_dec ? p.pmax_floats : 0) * 4;
-    S.in = reinterpret_cast<float*>(at);
-    at += DMAX * 32 * 4;
-    S.words = reinterpret_cast<uint32_t*>(at);
-    at += static_cast<size_t>(p.nmax) * 4;
-    S.col = reinterpret_cast<uint32_t*>(at);
-    at += static_cast<size_t>(32) * p.nwords * 4;
-    S.fix = reinterpret_cast<FixEntry*>(at);
-    return S;
-}
-
-template <int DMAX>
-size_t smem_bytes(const FusedProgram& p) {
-    return 128 + static_cast<size_t>(p.nmax) * DMAX * 4 + static_cast<size_t>(p.nmax) * 4 +
-           static_cast<size_t>(p.stage_dec ? p.pmax_floats : 0) * 4 + DMAX * 32 * 4 +
-           static_cast<size_t>(p.nmax) * 4 + static_cast<size_t>(32) * p.nwords * 4 + sizeof(FixEntry) * kFixCap;
+    tk.tick(FS_DECODE);
 }
 
 template <int DMAX, int BT, bool PROF>
-__global__ void __launch_bounds__(kThreads, 3) fused_run_kernel(FusedProgram p, int k_begin, int k_end) {
+__global__ void __launch_bounds__(kThreads, 2) fused_run_kernel(const __grid_constant__ FusedProgram p, int k_begin, int k_end) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(128) uint32_t smem[];
     const Smem S = carve<DMAX>(smem, p);
@@ -582,7 +715,7 @@ __global__ void __launch_bounds__(kThreads, 3) fused_run_kernel(FusedProgram p, 
     __syncthreads();
     uint32_t parity = 0;
     const int B = batch_of<BT>(p);
-    const int units = p.n_ens * p.btiles;
+    const int units = p.n_ens * p.groups;
     const int64_t gthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
     const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     Ticker<PROF> tk;
@@ -590,8 +723,9 @@ __global__ void __launch_bounds__(kThreads, 3) fused_run_kernel(FusedProgram p, 
 
     for (int k = k_begin; k < k_end; ++k) {
         const bool last = k == p.call_steps - 1;
+        if (gtid == 0) p.work[(k + 1) & 1] = 0;  // last used by step k-1; next used by step k+1
         // write_feeds (exec.cpp:313-326) into the arena: only the last step's
-        // values survive a call, and phase B reads fed sources from the feed block
+        // values survive a call; connections read fed sources from the feed block
         for (int f = 0; last && f < p.n_feeds; ++f) {
             if (!p.feed_present[f]) continue;
             const FFeed& fd = p.feeds[f];
@@ -603,54 +737,25 @@ __global__ void __launch_bounds__(kThreads, 3) fused_run_kernel(FusedProgram p, 
                 p.arena[fd.base + d * (fd.copies > 1 ? B : 1) + bb] = src[d * B + bb];
             }
         }
-        tk.tick(FS_FEED);
-        // phase A: units claimed dynamically (counter k & 1, reset a step ahead)
+        if (k > k_begin) grid_step_work<DMAX, BT>(p, k - 1, false, false);
+        tk.tick(FS_DEFER);
         int* work = p.work + (k & 1);
         for (;;) {
-            if (threadIdx.x == 0) *S.next_unit = atomicAdd(work, 1);
+            if (threadIdx.x == 0) *S.cur = atomicAdd(work, 1);
             __syncthreads();
-            const int u = *S.next_unit;
-            if (u >= units) break;  // uniform; the next write of next_unit follows a barrier inside the unit
-            phase_a_unit<DMAX, BT, PROF>(p, u, last, S, parity, tk);
+            const int u = *S.cur;
+            __syncthreads();  // every thread has read cur before thread 0 claims again
+            if (u >= units) break;  // uniform
+            run_unit<DMAX, BT, PROF>(p, u, k, k > k_begin, last, S, parity, tk);
             parity ^= 1u;
+            __syncthreads();  // staging buffers, words and queues are reused by the next unit
         }
         grid_sync(grid);
-        tk.tick(FS_BAR1);
-        if (gtid == 0) p.work[(k + 1) & 1] = 0;  // last used by step k-1; next used by step k+1
-        // phase B: connections (item = column-fastest, so a warp shares one
-        // connection when B % 32 == 0), then time and captures of phase-A values
-        const int64_t items = static_cast<int64_t>(p.n_conn) * B;
-        for (int64_t it = gtid; it < items; it += gthreads) {
-            const int c = static_cast<int>(it / B);
-            phase_b_item<DMAX, BT>(p, c, static_cast<int>(it - static_cast<int64_t>(c) * B), last, k);
-        }
-        for (int q = 0; q < p.n_probes; ++q) {
-            const FProbe& pr = p.probes[q];
-            const int64_t n = static_cast<int64_t>(pr.dim) * B;
-            float* dst = p.ring + p.ring_off[pr.index] + static_cast<int64_t>(k) * pr.dim * B;
-            const bool fed = pr.feed_slot >= 0 && p.feed_present[pr.feed_slot];
-            const float* fsrc = fed ? p.feed_data + p.feed_off[pr.feed_slot] + static_cast<int64_t>(k) * pr.dim * B
-                                    : nullptr;
-            for (int64_t i = gtid; i < n; i += gthreads) {
-                const int64_t d = i / B;
-                const int bb = static_cast<int>(i - d * B);
-                dst[i] = fed ? fsrc[d * B + (pr.per_batch ? bb : 0)] : p.arena[pr.base + (pr.per_batch ? d * B + bb : d)];
-            }
-        }
-        if (p.has_time && gtid == 0) {  // TimeUpdate (exec.cpp:300-309)
-            const float next = p.arena[p.step_base] + 1.0f;
-            p.arena[p.step_base] = next;
-            p.arena[p.time_base] = next * p.dt;
-            if (p.time_probe_step >= 0)
-                for (int bb = 0; bb < B; ++bb) p.ring[p.ring_off[p.time_probe_step] + static_cast<int64_t>(k) * B + bb] = next;
-            if (p.time_probe_time >= 0)
-                for (int bb = 0; bb < B; ++bb)
-                    p.ring[p.ring_off[p.time_probe_time] + static_cast<int64_t>(k) * B + bb] = next * p.dt;
-        }
-        tk.tick(FS_B);
-        grid_sync(grid);
-        tk.tick(FS_BAR2);
+        tk.tick(FS_BAR);
     }
+    // epilogue: connection updates, captures and clock of the launch's last step
+    grid_step_work<DMAX, BT>(p, k_end - 1, true, k_end - 1 == p.call_steps - 1);
+    tk.tick(FS_EPI);
     tk.flush(p.prof);
 }
 
@@ -709,6 +814,15 @@ int max_grid_d(const FusedProgram& p, int device) {
 }  // namespace
 
 int fused_dmax_for(int d) { return d <= 8 ? 8 : d <= 16 ? 16 : d <= 32 ? 32 : 0; }
+
+size_t fused_smem_bytes(const FusedProgram& p, int dmax) {
+    switch (dmax) {
+        case 8: return smem_bytes<8>(p);
+        case 16: return smem_bytes<16>(p);
+        case 32: return smem_bytes<32>(p);
+    }
+    return 0;
+}
 
 cudaError_t launch_fused(const FusedProgram& p, int dmax, int grid, int k0, int k1, cudaStream_t stream) {
     const bool prof = p.prof != nullptr;

@@ -1,15 +1,24 @@
 // fused.hpp — descriptors of the fused ensemble pipeline (host + device).
 //
-// A recognised ensemble network is advanced with two phases per step and one
-// grid barrier after each (fused.cu):
-//   A  per (ensemble, 32-column batch tile):
-//        in   = Reset payload + sum of incoming filtered values, plan order
-//        J    = bias + E.in (sequential in j);  LIF step on v, r;  spikes as bits
-//        xhat = Reset payload + sum over spiking i of D[r,i]*(amp/dt), i ascending
-//   B  per (connection, batch column):
-//        acc  = Reset payload + T.src (sequential);  state = filt = a*state + b*acc
-// J, out, in and acc never touch HBM except on the last step of a call (so the
-// arena holds the reference's full state at every call boundary).
+// A recognised ensemble network advances with ONE grid barrier per step
+// (fused.cu).  A unit is (ensemble, group of 32-column batch tiles); each warp
+// of the CTA owns one tile (and a slice of the neurons when a unit has fewer
+// tiles than warps).  For step k a unit
+//   1. applies the step k-1 update of every connection INTO its ensemble
+//      (destination side):  acc = Reset payload + T.src(k-1);
+//      state = filt = a*state + b*acc           (exec.cpp:226-240, 267-284)
+//      and sums in = Reset payload + filt_c in plan-group order (exec.cpp:189-210);
+//   2. sweeps its neurons: J = bias + E.in (sequential in j), lif_spike_step;
+//      neurons whose step needs a transcendental (a spike: log1p; leaving the
+//      refractory period: expm1) leave the sweep through warp queues and are
+//      resolved 32 at a time;
+//   3. decodes xhat = Reset payload + sum over spiking i (ascending) of
+//      D[r,i]*(amp/dt) into the step-parity buffer xbuf[k & 1].
+// The update of step k-1 for connections without a destination ensemble, the
+// probe captures of step k-1 and the clock run at the start of step k; the
+// launch's last step is completed by an epilogue after a final barrier.
+// J, out, in, acc and filt reach the arena on a call's last step only, so the
+// arena holds the reference's full state at every call boundary.
 #pragma once
 
 #include <cstdint>
@@ -20,13 +29,13 @@ namespace nengb {
 
 struct FEns {
     int64_t in_base, j_base, out_base, v_base, r_base, xhat_base;  // per-batch: element e, copy b at base + e*B + b
-    int64_t enc_base, dec_base;                                    // shared: E [n][d], D [dx][n] row-major
     int32_t n, d, dx;                                              // neurons, input dims, decoded dims
     int32_t n_pad;                                                 // n rounded up to 4 (bulk-copy granularity)
-    int32_t inc_begin, inc_count;                                  // incoming connections (plan order)
+    int32_t inc_begin, inc_count;                                  // incoming connections (plan order) in `incoming`
     int32_t in_init_off, xhat_init_off;                            // Reset payloads in `values`
+    int32_t xb_row;          // first row of this ensemble's xhat in the parity buffers
     int64_t bias_off;        // Reset(J) payload, n_pad floats (16-B aligned)
-    int64_t epad_off;        // encoders [n][DMAX], rows zero padded (16-B aligned)
+    int64_t epad_off;        // encoders [n (even)][DMAX], rows zero padded (16-B aligned)
     int64_t dec_scaled_off;  // fp32(D[r,i]) * fp32(amp/dt), transposed [n][dx] — the DotInc term of a spike
     int32_t dec_bytes;       // n*dx*4 rounded up to 16 (bulk-copy size)
     float dt, tau_rc, tau_ref, amplitude;
@@ -36,22 +45,23 @@ struct FEns {
 };
 
 struct FConn {
-    int64_t src_base;  // xhat of an ensemble or a fed node signal (per-batch)
-    int64_t t_base;    // shared T [dd][ds]
+    int64_t src_base;  // arena base of the source signal (an ensemble's xhat or a fed node)
     int64_t tpad_off;  // T rows zero padded to DMAX in `values` (16-B aligned)
     int64_t acc_base, filt_base, state_base;
     int32_t dd, ds;
-    int32_t src_feed;  // feed slot index when the source is a fed node (read from the staged feeds), else -1
+    int32_t src_xb;    // first parity-buffer row of the source ensemble's xhat, or -1
+    int32_t src_feed;  // feed slot index when the source is a fed node, else -1
     int32_t acc_init_off;
     int32_t probe_filt, probe_state;  // probe indices capturing filt / state, -1 none
     float a, b;                       // lowpass coefficients (f32 of the f64 values)
 };
 
-struct FProbe {  // capture of a value not written in phase B
+struct FProbe {  // capture of a value the units produce (xhat) or a fed node
     int64_t base;  // arena base of the signal
     int32_t dim, per_batch;
     int32_t index;      // probe index (ring slot)
     int32_t feed_slot;  // >= 0: a fed node's signal (captured from the staged feeds when present)
+    int32_t xb_row;     // >= 0: an ensemble's xhat (captured from the parity buffer)
 };
 
 struct FFeed {
@@ -65,11 +75,15 @@ struct FusedProgram {
     const float* values = nullptr;
     const FEns* ens = nullptr;
     const FConn* conns = nullptr;
-    const int64_t* incoming = nullptr;  // per ensemble, plan order: arena base of each incoming filter state
-    const FProbe* probes = nullptr;     // xhat / feed / other-phase-A-final captures
+    const int32_t* incoming = nullptr;  // per ensemble, plan order: connection indices
+    const int32_t* orphans = nullptr;   // connections with no destination ensemble
+    const FProbe* probes = nullptr;
     const FFeed* feeds = nullptr;
-    int32_t n_ens = 0, n_conn = 0, n_probes = 0, n_feeds = 0;
-    int32_t batch = 1, btiles = 1, nmax = 0, nwords = 0;
+    float* xbuf = nullptr;  // two parity buffers of xrows rows x B
+    int32_t n_ens = 0, n_conn = 0, n_orphans = 0, n_probes = 0, n_feeds = 0;
+    int32_t xrows = 0;
+    int32_t batch = 1, btiles = 1, nmax = 0;
+    int32_t tu = 8, slices = 1, groups = 1;  // tiles per unit, warps per tile, units per ensemble
     int32_t has_time = 0, time_probe_step = -1, time_probe_time = -1;
     int32_t stage_dec = 0;    // decoder products staged into shared memory (when they fit)
     int32_t pmax_floats = 0;  // max over ensembles of n*dx rounded up to 4
@@ -85,9 +99,9 @@ struct FusedProgram {
     int32_t call_steps = 0;
     // optional section timers (NENG_FUSED_PROFILE=1): per-CTA ns summed over CTAs
     unsigned long long* prof = nullptr;
-    int32_t* work = nullptr;  // two phase-A unit counters (step parity), zero at launch
+    int32_t* work = nullptr;  // two unit counters (step parity), zero at launch
 };
 
-enum FusedSection { FS_FEED, FS_A1, FS_A2, FS_FIX, FS_A3, FS_A4, FS_BAR1, FS_B, FS_BAR2, FS_COUNT };
+enum FusedSection { FS_DEFER, FS_IN, FS_SWEEP, FS_QUEUE, FS_FIX, FS_DECODE, FS_BAR, FS_EPI, FS_COUNT };
 
 }  // namespace nengb
