@@ -205,6 +205,19 @@ const LibmTables& libm_tables(int device) {
         size_t a = static_cast<size_t>(lo - ht.keys.begin()), b = static_cast<size_t>(hi - ht.keys.begin());
         build(ht.keys.data() + a, ht.results.data() + a, b > a ? b - a : 0, &dl->tables.t[t].hot_slots,
               &dl->tables.t[t].hot_mask, &dl->tables.t[t].hot_shift);
+        {
+            // block filter over k = key - 0x80000001 in [0, 0x3D800000): bit (k >> 6)
+            std::vector<uint32_t> filt((0x3D800000u >> 11) + 1, 0u);
+            for (size_t q = a; q < b; ++q) {
+                const uint32_t k = ht.keys[q] - 0x80000001u;
+                filt[k >> 11] |= 1u << ((k >> 6) & 31u);
+            }
+            void* df = nullptr;
+            cuda_check(cudaMalloc(&df, filt.size() * 4), "cudaMalloc libm filter");
+            cuda_check(cudaMemcpy(df, filt.data(), filt.size() * 4, cudaMemcpyHostToDevice), "libm filter H2D");
+            dl->allocs.push_back(df);
+            dl->tables.t[t].hot_filter = static_cast<const uint32_t*>(df);
+        }
         // skip lookups whose double result is farther than this from a float
         // rounding midpoint (all exceptions are closer); margin covers the
         // device/host double results differing by a few double ulps
@@ -229,6 +242,14 @@ const LibmTables& libm_tables(int device) {
         cuda_check(cudaMemcpy(dwin, win.data(), win.size() * 4, cudaMemcpyHostToDevice), "libm windows H2D");
         dl->allocs.push_back(dwin);
         dl->tables.t[t].region_win = static_cast<const uint32_t*>(dwin);
+        // byte screen for shared memory: doubtful when (d >> 21) <= w8 (d <= win implies it)
+        std::vector<uint8_t> w8(win.size());
+        for (size_t i = 0; i < win.size(); ++i) w8[i] = static_cast<uint8_t>(std::min<uint32_t>(win[i] >> 21, 255u));
+        void* dw8 = nullptr;
+        cuda_check(cudaMalloc(&dw8, std::max<size_t>(w8.size(), 16)), "cudaMalloc libm byte windows");
+        cuda_check(cudaMemcpy(dw8, w8.data(), w8.size(), cudaMemcpyHostToDevice), "libm byte windows H2D");
+        dl->allocs.push_back(dw8);
+        dl->tables.t[t].region_w8 = static_cast<const uint8_t*>(dw8);
         dl->tables.t[t].region_shift = ht.region_shift;
         dl->tables.t[t].n_regions = static_cast<uint32_t>(reg.size());
     }

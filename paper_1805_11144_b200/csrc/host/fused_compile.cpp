@@ -55,7 +55,7 @@ class FusedImpl : public FusedPlan {
   public:
     FusedProgram prog;
     int dmax = 8, grid = 1, steps_per_launch = 0;
-    DevMem d_ens, d_conns, d_incoming, d_orphans, d_values, d_probes, d_feeds, d_call, d_prof, d_work, d_xbuf;
+    DevMem d_ens, d_conns, d_incoming, d_orphans, d_values, d_probes, d_feeds, d_call, d_prof, d_work, d_xbuf, d_dq;
     std::string desc;
 
     int64_t run(int n_steps, const float* d_feed_data, const int64_t* feed_off, const int* present, float* d_ring,
@@ -102,7 +102,7 @@ class FusedImpl : public FusedPlan {
             for (int s = 0; s < FS_COUNT; ++s)
                 std::fprintf(stderr, " %s=%.1f", names[s], h[s] / 1e3 / grid / n_steps);
             std::fprintf(stderr, " (total %.1f)\n", tot / 1e3 / grid / n_steps);
-            std::fprintf(stderr, "[fused profile] per step: exit batches %.0f, spike batches %.0f, doubt batches %.0f, doubt entries %.0f\n",
+            std::fprintf(stderr, "[fused profile] per step: doubts exit %.0f, spike out-of-range %.0f, spike window %.0f, doubt entries %.0f\n",
                          double(h[FS_COUNT]) / n_steps, double(h[FS_COUNT + 1]) / n_steps, double(h[FS_COUNT + 2]) / n_steps,
                          double(h[FS_COUNT + 3]) / n_steps);
         }
@@ -528,6 +528,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         p.btiles = (B + 31) / 32;
         p.nmax = (nmax + 31) / 32 * 32;
         p.pmax_floats = pmax_floats;
+        p.libm = libm_tables(eng.device());
         // tiles per unit (one warp each) and warps per tile (neuron slices)
         {
             int tu = 1;
@@ -552,7 +553,6 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             p.step_base = eng.resolve_full(m.operators[time_op].operands[0].signal).base;
             p.time_base = eng.resolve_full(m.operators[time_op].operands[1].signal).base;
         }
-        p.libm = libm_tables(eng.device());
         impl->steps_per_launch = eng.steps_per_launch();
         impl->n_probe_total = static_cast<int>(m.probes.size());
         impl->dmax = fused_dmax_for(dmax_need);
@@ -561,6 +561,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         int64_t work = std::max<int64_t>(static_cast<int64_t>(p.n_ens) * p.groups,
                                          (static_cast<int64_t>(p.n_conn) * B + 255) / 256);
         impl->grid = static_cast<int>(std::min<int64_t>(cap, std::max<int64_t>(1, work)));
+
         std::ostringstream os;
         os << "fused: " << p.n_ens << " ensembles, " << p.n_conn << " connections, dmax " << impl->dmax << ", grid "
            << impl->grid << ", tiles/unit " << p.tu << ", slices " << p.slices << ", stage_dec " << p.stage_dec

@@ -51,8 +51,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kUnroll = 8;   // neuron rows per prefetch round (pairs inside)
 constexpr int kL2Ahead = 24; // rows of v/r pulled into L2 ahead of the round being computed
 constexpr uint32_t kFull = 0xffffffffu;
-// per-warp doubt queue capacity: <= 31 pending + 64 from a neuron pair
-constexpr int kQEntries = 96;
+
 
 __device__ __forceinline__ void grid_sync(cg::grid_group& g) {
     if (gridDim.x == 1)
@@ -141,6 +140,7 @@ struct __align__(16) QEnt {
     uint32_t key;  // neuron << 5 | lane
     float a, b, c; // the step's original v, r, J
 };
+constexpr int kDQ = 96;  // per-warp doubt queue: <= 31 pending + 64 from a neuron pair
 
 struct Smem {
     uint64_t* bar;
@@ -150,9 +150,17 @@ struct Smem {
     float* P;      // decoder products [n][dx] (when p.stage_dec)
     float* in;     // tu x DMAX x 32
     uint32_t* words;  // tu x nmax: spike ballot of neuron i in tile slot t (bit = lane)
-    QEnt* q;          // kWarps x kQEntries
     float* ring;      // kWarps x [2 stages][v, r][kUnroll rows][32]
+    QEnt* dq;         // kWarps x kDQ doubt entries
+    uint8_t* w8e;     // byte screening windows per region (expm1, log1p), see libm_w8_bytes
+    uint8_t* w8l;
 };
+
+/// Bytes of one shared-memory copy of a region byte table (rounded to 16).
+__host__ __device__ __forceinline__ size_t libm_w8_bytes(const LibmTables& t) {
+    return (static_cast<size_t>(t.t[0].n_regions > t.t[1].n_regions ? t.t[0].n_regions : t.t[1].n_regions) + 15) &
+           ~static_cast<size_t>(15);
+}
 
 constexpr int kRingFloats = 2 * 2 * kUnroll * 32;  // per warp
 
@@ -165,6 +173,12 @@ __device__ Smem carve(uint32_t* base, const FusedProgram& p) {
     at += 128;
     S.ring = reinterpret_cast<float*>(at);
     at += static_cast<size_t>(kWarps) * kRingFloats * 4;
+    S.dq = reinterpret_cast<QEnt*>(at);
+    at += sizeof(QEnt) * kDQ * kWarps;
+    S.w8e = reinterpret_cast<uint8_t*>(at);
+    at += libm_w8_bytes(p.libm);
+    S.w8l = reinterpret_cast<uint8_t*>(at);
+    at += libm_w8_bytes(p.libm);
     S.E = reinterpret_cast<float*>(at);
     at += static_cast<size_t>(p.nmax) * DMAX * 4;
     S.bias = reinterpret_cast<float*>(at);
@@ -175,16 +189,15 @@ __device__ Smem carve(uint32_t* base, const FusedProgram& p) {
     at += static_cast<size_t>(p.tu) * DMAX * 32 * 4;
     S.words = reinterpret_cast<uint32_t*>(at);
     at += static_cast<size_t>(p.tu) * p.nmax * 4;
-    S.q = reinterpret_cast<QEnt*>(at);
     return S;
 }
 
 template <int DMAX>
 size_t smem_bytes(const FusedProgram& p) {
-    return 128 + static_cast<size_t>(kWarps) * kRingFloats * 4 + static_cast<size_t>(p.nmax) * DMAX * 4 +
+    return 128 + static_cast<size_t>(kWarps) * kRingFloats * 4 + 2 * libm_w8_bytes(p.libm) + sizeof(QEnt) * kDQ * kWarps +
+           static_cast<size_t>(p.nmax) * DMAX * 4 +
            static_cast<size_t>(p.nmax) * 4 + static_cast<size_t>(p.stage_dec ? p.pmax_floats : 0) * 4 +
-           static_cast<size_t>(p.tu) * DMAX * 32 * 4 + static_cast<size_t>(p.tu) * p.nmax * 4 +
-           sizeof(QEnt) * kQEntries * kWarps;
+           static_cast<size_t>(p.tu) * DMAX * 32 * 4 + static_cast<size_t>(p.tu) * p.nmax * 4;
 }
 
 /// The batch width: BT when the kernel is specialised for it (row strides then
@@ -214,34 +227,76 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-/// Copy rows [i, i + kUnroll) (those below n1) of v and r, columns [b0, b0 + 32)
-/// of this tile, into ring stage `st`.  vec: 16-B chunks (B % 4 == 0), else 4-B.
-__device__ __forceinline__ void ring_issue(float* ring, int st, const float* vrow0, const float* rrow0, int i, int n1,
-                                           int B, int b0, int lane, bool vec) {
-    float* dst = ring + st * (2 * kUnroll * 32);
-    if (vec) {
-        const int c4 = (lane & 7) * 4;
-        if (b0 + c4 < B) {
+__device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4_s(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+
+/// A lane's share of the ring copies, precomputed once per sweep.  vec (B % 4
+/// == 0): lane copies 16 B, columns c4..c4+3 of rows (lane >> 3) and
+/// (lane >> 3) + 4 of each 8-row round; else 4 B (its own column) of all 8 rows.
+struct RingLane {
+    const float* src;  // v element (row n0 + lane-row, column b0 + lane-col)
+    int64_t rdelta;    // r_base - v_base
+    uint32_t dst;      // shared address of the lane's first element in stage 0
+    int row;           // first row of the round this lane copies
+    bool ok;           // the lane's columns exist
+};
+
+/// Copy the round starting at row i (rows below n1) of v and r into stage st.
+template <int BT>
+__device__ __forceinline__ void ring_issue(const RingLane& L, int st, int i, int n0, int n1, int B, bool vec) {
+    const int64_t Bs = BT > 0 ? BT : B;
+    const float* src = L.src + static_cast<int64_t>(i - n0) * Bs;
+    const uint32_t dst = L.dst + st * (kUnroll * 32 * 4);
+    if (L.ok) {
+        if (vec) {
 #pragma unroll
-            for (int a = 0; a < 2; ++a)
-#pragma unroll
-                for (int h = 0; h < kUnroll / 4; ++h) {
-                    const int rr = 4 * h + (lane >> 3);
-                    if (i + rr < n1)
-                        cp_async16(dst + (a * kUnroll + rr) * 32 + c4,
-                                   (a ? rrow0 : vrow0) + static_cast<int64_t>(i + rr) * B + c4);
+            for (int h = 0; h < kUnroll / 4; ++h)
+                if (i + L.row + 4 * h < n1) {
+                    cp_async16_s(dst + h * 4 * 32 * 4, src + 4 * h * Bs);
+                    cp_async16_s(dst + h * 4 * 32 * 4 + 2 * kUnroll * 32 * 4, src + 4 * h * Bs + L.rdelta);
                 }
-        }
-    } else if (b0 + lane < B) {
-#pragma unroll
-        for (int a = 0; a < 2; ++a)
+        } else {
 #pragma unroll
             for (int rr = 0; rr < kUnroll; ++rr)
-                if (i + rr < n1)
-                    cp_async4(dst + (a * kUnroll + rr) * 32 + lane,
-                              (a ? rrow0 : vrow0) + static_cast<int64_t>(i + rr) * B + lane);
+                if (i + rr < n1) {
+                    cp_async4_s(dst + rr * 32 * 4, src + rr * Bs);
+                    cp_async4_s(dst + rr * 32 * 4 + 2 * kUnroll * 32 * 4, src + rr * Bs + L.rdelta);
+                }
+        }
     }
     cp_async_commit();
+}
+
+/// The speculative LIF-range evaluation of libm.cuh (spec_expm1 / spec_log1p)
+/// with the per-region screen read from the shared-memory byte table:
+/// doubtful when |low29 - 2^28| >> 21 <= w8 (a superset of the exact window,
+/// so every value the exact screen flags is flagged here too).
+__device__ __forceinline__ Spec spec_smem(float x, bool is_log, const uint8_t* w8, uint32_t shift) {
+    const double y = is_log ? log1p_fast(static_cast<double>(x)) : expm1_fast(static_cast<double>(x));
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(y));
+    const uint32_t hi = static_cast<uint32_t>(u >> 32), lo = static_cast<uint32_t>(u);
+    const bool den = (hi & 0x7FF00000u) < (897u << 20);  // |y| < 2^-126: float-denormal result
+    const uint32_t d = static_cast<uint32_t>(abs(static_cast<int>(lo & 0x1FFFFFFFu) - 0x10000000));
+    const uint32_t w = w8[(__float_as_uint(x) - 0x80000000u) >> shift];
+    return {static_cast<float>(y), den || (d >> 21) <= w};
+}
+
+/// spec_smem for any x: `doubtful` also when x is outside the LIF range (the
+/// polynomial is then meaningless and the exact path takes over).
+__device__ __forceinline__ Spec spec_any(float x, bool is_log, const uint8_t* w8, uint32_t shift) {
+    const uint32_t k = __float_as_uint(x) - 0x80000001u;  // x in [-1/16, 0) <=> k <= 0x3D7FFFFF
+    const bool inr = k <= 0x3D7FFFFFu;
+    const double y = is_log ? log1p_fast(static_cast<double>(x)) : expm1_fast(static_cast<double>(x));
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(y));
+    const uint32_t hi = static_cast<uint32_t>(u >> 32), lo = static_cast<uint32_t>(u);
+    const bool den = (hi & 0x7FF00000u) < (897u << 20);  // |y| < 2^-126: float-denormal result
+    const uint32_t d = static_cast<uint32_t>(abs(static_cast<int>(lo & 0x1FFFFFFFu) - 0x10000000));
+    const uint32_t w = w8[min(k + 1u, 0x3D800000u) >> shift];
+    return {static_cast<float>(y), !inr || den || (d >> 21) <= w};
 }
 
 /// lif_spike_step<float> resolved exactly (table probes as needed); returns
@@ -264,9 +319,10 @@ __device__ __forceinline__ bool lif_exact(float J, float& v, float& r, float dt,
     return false;
 }
 
-/// Doubtful values (out of line: ~5% of transcendentals): lif_spike_step
+/// Doubtful values (out of line: ~5% of the transcendentals): lif_spike_step
 /// recomputed exactly from the original v, r, J; patches v, r and the spike
-/// bit.  Lane l takes entry l of q[0, cnt).
+/// bit.  Lane l takes entry l of q[0, cnt).  Called from the sweep every 32
+/// entries, so its latency overlaps the other warps' sweeps.
 __device__ __noinline__ void dq_batch(const QEnt* q, int cnt, const FEns* e, float* A, int B, int b0,
                                       uint32_t* words, const LibmTables* lt, int lane) {
     if (lane >= cnt) return;
@@ -476,9 +532,9 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
     const int nper = ((e.n + p.slices - 1) / p.slices + 31) & ~31;
     const int n0 = min(e.n, slice * nper), n1 = min(e.n, n0 + nper);
     uint32_t* words = S.words + tslot * p.nmax;
+    QEnt* dq = S.dq + warp * kDQ;
+    int dn = 0;
     if (active && n0 < n1) {
-        QEnt* dq = S.q + warp * kQEntries;
-        int dn = 0;
         const float dt = e.dt, em_dt = e.em_dt, tau_rc = e.tau_rc, tau_ref = e.tau_ref;
         const double inv_tau_rc = e.inv_tau_rc;
         const float2 dt2 = make_float2(dt, dt), ndt2 = make_float2(-dt, -dt);
@@ -497,13 +553,27 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
         const float* pf_base = (pf_rows || lane < kUnroll) ? pf_v : pf_r;
         float* vst = vrow0 + static_cast<int64_t>(n0) * B + lane;  // row i of this lane
         const int64_t rdelta = e.r_base - e.v_base;
-        ring_issue(ring, 0, vrow0, rrow0, n0, n1, B, b0, lane, vec);
-        for (int i = n0; i < n1; i += 2, vst += 2 * B) {
+        RingLane RL;
+        {
+            const int lr = vec ? (lane >> 3) : 0, lc = vec ? (lane & 7) * 4 : lane;
+            RL.src = vrow0 + static_cast<int64_t>(n0 + lr) * B + lc;
+            RL.rdelta = rdelta;
+            RL.dst = smem_addr(ring + lr * 32 + lc);
+            RL.row = lr;
+            RL.ok = b0 + lc < B;
+        }
+        ring_issue<BT>(RL, 0, n0, n0, n1, B, vec);
+        const bool lv = (BT > 0 && BT % 32 == 0) ? true : valid;  // inside the sweep the tile is active
+        const uint32_t sh_e = lt.t[0].region_shift, sh_l = lt.t[1].region_shift;
+        const float* ring_l = ring + lane;
+        const float* sE = S.E + n0 * DMAX;
+        const float* sbias = S.bias + n0;
+        for (int i = n0; i < n1; i += 2, vst += 2 * B, sE += 2 * DMAX, sbias += 2) {
             const int rel = i - n0;
-            const int st = (rel >> 3) & 1, rr = rel & (kUnroll - 1);
-            if (rr == 0) {
+            if ((rel & (kUnroll - 1)) == 0) {
+                const int st = (rel >> 3) & 1;
                 __syncwarp();  // every lane's reads of the stage being refilled are done
-                ring_issue(ring, st ^ 1, vrow0, rrow0, i + kUnroll, n1, B, b0, lane, vec);
+                ring_issue<BT>(RL, st ^ 1, i + kUnroll, n0, n1, B, vec);
                 cp_async_wait1();
                 __syncwarp();
                 const int pi = i + kL2Ahead;
@@ -521,9 +591,9 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
                     }
                 }
             }
-            const float* sv = ring + st * (2 * kUnroll * 32) + rr * 32 + lane;
+            const float* sv = ring_l + (rel & (2 * kUnroll - 1)) * 32;
             const float2 v2 = make_float2(sv[0], sv[32]);
-            const float2 r2 = make_float2(sv[kUnroll * 32], sv[kUnroll * 32 + 32]);
+            const float2 r2 = make_float2(sv[2 * kUnroll * 32], sv[2 * kUnroll * 32 + 32]);
             // DotInc(E, in, J) for neurons i, i+1: acc from +0, j ascending, then J = bias + acc.
             // Products two dims at a time (FMUL2), sums scalar and in order.  A
             // paired product must never feed a paired sum: ptxas contracts
@@ -531,7 +601,7 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
             float acc[2];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const float4* er = reinterpret_cast<const float4*>(S.E + (i + h) * DMAX);
+                const float4* er = reinterpret_cast<const float4*>(sE + h * DMAX);
                 float a = 0.0f;
 #pragma unroll
                 for (int q = 0; q < DMAX / 4; ++q) {
@@ -545,7 +615,7 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
                 }
                 acc[h] = a;
             }
-            const float2 J2 = __fadd2_rn(*reinterpret_cast<const float2*>(S.bias + i), make_float2(acc[0], acc[1]));
+            const float2 J2 = __fadd2_rn(*reinterpret_cast<const float2*>(sbias), make_float2(acc[0], acc[1]));
             const float2 dl2 = __fadd2_rn(dt2, make_float2(-r2.x, -r2.y));  // dt - r
             const float2 rr2 = __fadd2_rn(r2, ndt2);                        // r - dt
             // lif_spike_step<float> (neuron_math.hpp:55-77) with both transcendentals
@@ -554,20 +624,19 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
             // rounded, exact unless `doubtful`; doubtful or out-of-range lanes are
             // recomputed exactly in the doubt queue from their original v, r, J.
             float em[2];
-            bool ex[2], dbt[2];
+            bool dbt[2];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const float delta = h ? dl2.y : dl2.x;  // clamp to [0, dt] below, NaN kept
                 const bool ge = delta >= dt, le = delta <= 0.0f;
-                ex[h] = !ge && !le;  // 0 < delta < dt (or NaN): the step leaving the refractory period
+                const bool ex = !ge && !le;  // 0 < delta < dt (or NaN): the step leaving the refractory period
                 // == -delta / tau_rc in IEEE float: the double product is within 2^-52 of the quotient,
                 // and a quotient of floats is never within 2^-49 of a float midpoint unless on it,
                 // which needs a power-of-two divisor (then the product is exact)
                 const float xa = static_cast<float>(static_cast<double>(-delta) * inv_tau_rc);
-                const bool in_a = ex[h] && lif_range(xa);
-                const Spec sa = spec_expm1(in_a ? xa : -0.025f, lt);
-                em[h] = ex[h] ? sa.r : (ge ? em_dt : -0.0f);  // expm1(-dt/tau_rc) from the host; expm1(-0) = -0
-                dbt[h] = ex[h] && (!in_a || sa.doubtful);
+                const Spec sa = spec_any(xa, false, S.w8e, sh_e);
+                em[h] = ex ? sa.r : (ge ? em_dt : -0.0f);  // expm1(-dt/tau_rc) from the host; expm1(-0) = -0
+                dbt[h] = ex && sa.doubtful;
             }
             // v - (J - v) * em: scalar products between the paired sums (see above)
             const float2 d2 = __fadd2_rn(J2, make_float2(-v2.x, -v2.y));
@@ -576,52 +645,42 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
             const bool two = i + 1 < n1;  // warp-uniform
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const bool row = h == 0 || two;
+                const bool row = lv && (h == 0 || two);
                 const float J = h ? J2.y : J2.x, vh = h ? v2.y : v2.x, rh = h ? r2.y : r2.x;
                 float vn = h ? vn2.y : vn2.x;
                 if (vn < 0.0f) vn = 0.0f;
                 const bool spike = vn > 1.0f;
                 const float xl = -(vn - 1.0f) / (J - 1.0f);
-                const bool in_l = spike && lif_range(xl);
-                const Spec sl = spec_log1p(in_l ? xl : -0.01f, lt);
-                const bool d = row && valid && (dbt[h] || (spike && (!in_l || sl.doubtful)));
+                const Spec sl = spec_any(xl, true, S.w8l, sh_l);
+                const bool d = row && (dbt[h] || (spike && sl.doubtful));
                 const float since = -tau_rc * sl.r;
                 const float rn = spike ? tau_ref - since : (rh > dt ? (h ? rr2.y : rr2.x) : 0.0f);
-                if (row && valid && !d) {
+                if (row && !d) {  // doubtful lanes are written by the resolution
                     __stcs(vst + h * B, spike ? 0.0f : vn);
                     __stcs(vst + h * B + rdelta, rn);
                 }
-                const uint32_t word = __ballot_sync(kFull, row && valid && spike);
-                if (row && lane == 0) words[i + h] = word;
+                const uint32_t word = __ballot_sync(kFull, row && spike);
+                if (lane == 0 && (h == 0 || two)) words[i + h] = word;
                 const uint32_t dm = __ballot_sync(kFull, d);
                 if (dm) {  // warp-uniform
                     if (d) dq[dn + __popc(dm & lanemask_lt())] = QEnt{(static_cast<uint32_t>(i + h) << 5) | lane, vh, rh, J};
                     dn += __popc(dm);
                 }
             }
-            if (dn >= 32) {
+            if (dn >= 32) {  // warp-uniform
                 dn -= 32;
                 __syncwarp();
-                if constexpr (PROF) {
-                    if (lane == 0) {
-                        atomicAdd(p.prof + FS_COUNT + 2, 1ull);
-                        atomicAdd(p.prof + FS_COUNT + 3, 32ull);
-                    }
-                }
+                tk.tick(FS_SWEEP);
                 dq_batch(dq + dn, 32, p.ens + ei, A, B, b0, words, &p.libm, lane);
                 __syncwarp();
+                tk.tick(FS_FIX);
             }
         }
         if (dn > 0) {
             __syncwarp();
-            if constexpr (PROF) {
-                if (lane == 0) {
-                    atomicAdd(p.prof + FS_COUNT + 2, 1ull);
-                    atomicAdd(p.prof + FS_COUNT + 3, static_cast<unsigned long long>(dn));
-                }
-            }
             dq_batch(dq, dn, p.ens + ei, A, B, b0, words, &p.libm, lane);
             __syncwarp();
+            dn = 0;
         }
         // the call's last step leaves J in the arena (DotInc(E, in, J) as above, once)
         if (last && valid) {
@@ -712,6 +771,8 @@ __global__ void __launch_bounds__(kThreads, 2) fused_run_kernel(const __grid_con
     extern __shared__ __align__(128) uint32_t smem[];
     const Smem S = carve<DMAX>(smem, p);
     if (threadIdx.x == 0) mbar_init(S.bar);
+    for (uint32_t i = threadIdx.x; i < p.libm.t[0].n_regions; i += blockDim.x) S.w8e[i] = p.libm.t[0].region_w8[i];
+    for (uint32_t i = threadIdx.x; i < p.libm.t[1].n_regions; i += blockDim.x) S.w8l[i] = p.libm.t[1].region_w8[i];
     __syncthreads();
     uint32_t parity = 0;
     const int B = batch_of<BT>(p);

@@ -100,6 +100,8 @@ struct FusedProgram {
     // optional section timers (NENG_FUSED_PROFILE=1): per-CTA ns summed over CTAs
     unsigned long long* prof = nullptr;
     int32_t* work = nullptr;  // two unit counters (step parity), zero at launch
+    void* dq = nullptr;       // per-warp doubt lists (16-B entries), resolved after each unit's decode
+    int32_t dq_cap = 0;       // entries per warp
 };
 
 enum FusedSection { FS_DEFER, FS_IN, FS_SWEEP, FS_QUEUE, FS_FIX, FS_DECODE, FS_BAR, FS_EPI, FS_COUNT };

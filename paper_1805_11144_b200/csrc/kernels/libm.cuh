@@ -80,8 +80,10 @@ __device__ __forceinline__ float region_from(const LibmHash& h, uint32_t key) {
 // exception lies inside).  Inside the window the rounded polynomial value is
 // glibc's unless the input is in the table: the generator records every
 // LIF-range input where the two differ, exceptions or not.
-__device__ __forceinline__ double expm1_fast(double x) { return neng_expm1_fast(x); }
-__device__ __forceinline__ double log1p_fast(double x) { return neng_log1p_fast(x); }
+static __constant__ double kExpm1FastC[NENG_EXPM1_FAST_N] = NENG_EXPM1_FAST_C;
+static __constant__ double kLog1pFastC[NENG_LOG1P_FAST_N] = NENG_LOG1P_FAST_C;
+__device__ __forceinline__ double expm1_fast(double x) { return neng_poly_fast(x, kExpm1FastC, NENG_EXPM1_FAST_N); }
+__device__ __forceinline__ double log1p_fast(double x) { return neng_poly_fast(x, kLog1pFastC, NENG_LOG1P_FAST_N); }
 
 /// True when y lies within `win` x 2^-29 float ulps of a float rounding
 /// midpoint (the low 29 mantissa bits of a double are the position between
@@ -162,6 +164,12 @@ __device__ __forceinline__ float glibc_log1pf(float x, const LibmTables& t) {
 
 /// Whether key is listed in the LIF-range table (an exception, or an input
 /// where the speculative polynomial rounds differently from glibc).
+/// The block filter: false means key is certainly not in the LIF-range table.
+__device__ __forceinline__ bool hot_maybe(const LibmHash& h, uint32_t key) {
+    const uint32_t k = key - 0x80000001u;  // key in the LIF range (callers check)
+    return (__ldg(h.hot_filter + (k >> 11)) >> ((k >> 6) & 31u)) & 1u;
+}
+
 __device__ __forceinline__ bool hot_listed(const LibmHash& h, uint32_t key) {
     uint32_t i = (key * 0x9E3779B1u) >> h.hot_shift;
     for (;;) {
@@ -178,7 +186,9 @@ __device__ __forceinline__ bool hot_listed(const LibmHash& h, uint32_t key) {
 __device__ __forceinline__ float glibc_spec_resolved(float x, bool is_log, const LibmTables& t) {
     if (lif_range(x)) {
         const Spec s = spec_lif(x, is_log, t);
-        if (!s.doubtful || !hot_listed(t.t[is_log ? 1 : 0], __float_as_uint(x))) return s.r;
+        if (!s.doubtful || !hot_maybe(t.t[is_log ? 1 : 0], __float_as_uint(x)) ||
+            !hot_listed(t.t[is_log ? 1 : 0], __float_as_uint(x)))
+            return s.r;
     }
     return is_log ? glibc_log1pf(x, t) : glibc_expm1f(x, t);
 }

@@ -82,6 +82,11 @@ struct LibmHash {
     // per-region bounds on [-1/16, 0): region = (key - 0x80000000) >> region_shift
     const float* region_from = nullptr;
     const uint32_t* region_win = nullptr;  // screening half-window per region, units of 2^-29 float ulp
+    const uint8_t* region_w8 = nullptr;    // region_win >> 21 (floor): the byte screen (d >> 21) <= w8 is a superset
+    // one bit per 64 consecutive LIF-range keys: set when the block holds a
+    // hot-table key (2 MB, L2-resident); a clear bit answers "not listed"
+    // without probing the hash table
+    const uint32_t* hot_filter = nullptr;
     uint32_t region_shift = 31;
     uint32_t n_regions = 0;
 };
