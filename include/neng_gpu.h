@@ -158,7 +158,12 @@ typedef struct neng_device_cfg {
     int32_t device;            /* CUDA ordinal */
     int32_t mode;              /* NENG_MODE_* */
     int32_t steps_per_launch;  /* K steps per persistent launch; 0 = engine default */
-    int32_t reserved[5];
+    /* Ensemble sharding (fused pipeline only; shard_count 0 or 1 = unsharded):
+     * this engine owns shard shard_rank of shard_count contiguous ensemble
+     * ranges and the connections into them; the caller all-gathers the xhat
+     * parity buffer between per-step calls (neng_gpu_call_*). */
+    int32_t shard_rank, shard_count;
+    int32_t reserved[3];
 } neng_device_cfg;
 
 typedef struct neng_engine neng_engine;
@@ -185,6 +190,28 @@ neng_status neng_gpu_run(neng_engine* e, int32_t n_steps, int32_t n_feeds,
 neng_status neng_gpu_run_device(neng_engine* e, int32_t n_steps, const float* const* d_feeds,
                                 float* const* d_probes, void* stream);
 neng_status neng_gpu_synchronize(neng_engine* e);
+
+/* Stepped device-resident call (the building block of sharded runs; same
+ * buffers and packing as neng_gpu_run_device):
+ *   neng_gpu_call_begin(e, n, feeds, probes, stream)
+ *   for k in [0, n): neng_gpu_call_step(e, k, k ? NENG_STEP_FIRST_UPDATE : 0)
+ *                    ... all-gather xhat parity buffer k & 1 across shards ...
+ *   neng_gpu_call_step(e, n, NENG_STEP_EPILOGUE)   (completes step n - 1)
+ *   neng_gpu_call_end(e)
+ * Bits and state are those of one neng_gpu_run_device call. */
+enum { NENG_STEP_FIRST_UPDATE = 1, NENG_STEP_EPILOGUE = 2 };
+neng_status neng_gpu_call_begin(neng_engine* e, int32_t n_steps, const float* const* d_feeds, float* const* d_probes,
+                                void* stream);
+neng_status neng_gpu_call_step(neng_engine* e, int32_t k, int32_t flags);
+neng_status neng_gpu_call_end(neng_engine* e);
+
+/* The fused pipeline's xhat parity buffers: 2 x xbuf_floats/2 floats (parity p
+ * at xbuf + p * xbuf_floats / 2); shard r's rows are the rank_floats floats at
+ * r * rank_floats within a parity buffer (an in-place all-gather layout). */
+neng_status neng_gpu_shard_layout(const neng_engine* e, int64_t* xbuf_floats, int64_t* rank_floats, float** xbuf);
+/* Use a caller-owned device buffer (>= xbuf_floats floats) for the parity
+ * buffers, e.g. one a collective library writes into. */
+neng_status neng_gpu_set_xhat_buffer(neng_engine* e, float* d_buf);
 
 neng_status neng_gpu_reset(neng_engine* e);
 

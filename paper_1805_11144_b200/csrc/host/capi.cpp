@@ -76,6 +76,36 @@ neng_status neng_gpu_run_device(neng_engine* e, int32_t n_steps, const float* co
     });
 }
 
+neng_status neng_gpu_call_begin(neng_engine* e, int32_t n_steps, const float* const* d_feeds, float* const* d_probes,
+                                void* stream) {
+    if (!e) return NENG_INVALID_ARGUMENT;
+    return guarded(&e->impl, [&] {
+        e->impl.call_begin(n_steps, d_feeds, d_probes, static_cast<cudaStream_t>(stream));
+    });
+}
+
+neng_status neng_gpu_call_step(neng_engine* e, int32_t k, int32_t flags) {
+    if (!e) return NENG_INVALID_ARGUMENT;
+    return guarded(&e->impl, [&] { e->impl.call_step(k, flags); });
+}
+
+neng_status neng_gpu_call_end(neng_engine* e) {
+    if (!e) return NENG_INVALID_ARGUMENT;
+    return guarded(&e->impl, [&] { e->impl.call_end(); });
+}
+
+neng_status neng_gpu_shard_layout(const neng_engine* e, int64_t* xbuf_floats, int64_t* rank_floats, float** xbuf) {
+    if (!e) return NENG_INVALID_ARGUMENT;
+    return guarded(const_cast<nengb::Engine*>(&e->impl), [&] {
+        e->impl.shard_layout(xbuf_floats, rank_floats, xbuf);
+    });
+}
+
+neng_status neng_gpu_set_xhat_buffer(neng_engine* e, float* d_buf) {
+    if (!e) return NENG_INVALID_ARGUMENT;
+    return guarded(&e->impl, [&] { e->impl.set_xhat_buffer(d_buf); });
+}
+
 neng_status neng_gpu_synchronize(neng_engine* e) {
     if (!e) return NENG_INVALID_ARGUMENT;
     return guarded(&e->impl, [&] { e->impl.synchronize(); });

@@ -279,7 +279,14 @@ Engine::Engine(PlannedModel planned, int batch, int unroll, const neng_device_cf
         device_ = cfg->device;
         requested_mode_ = cfg->mode;
         steps_per_launch_ = cfg->steps_per_launch;
+        shard_rank_ = cfg->shard_rank;
+        shard_count_ = cfg->shard_count > 0 ? cfg->shard_count : 1;
     }
+    if (shard_count_ < 1 || shard_rank_ < 0 || shard_rank_ >= shard_count_)
+        throw BuildError("shard rank " + std::to_string(shard_rank_) + " is outside [0, " +
+                         std::to_string(shard_count_) + ")");
+    if (shard_count_ > 1 && requested_mode_ == NENG_MODE_GENERIC)
+        throw BuildError("ensemble sharding needs the fused pipeline");
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
     compile();
@@ -377,7 +384,7 @@ void Engine::compile() {
         fused_ = try_compile_fused(*this, &why);
         if (fused_)
             mode_ = NENG_MODE_FUSED;
-        else if (requested_mode_ == NENG_MODE_FUSED)
+        else if (requested_mode_ == NENG_MODE_FUSED || shard_count_ > 1)
             throw BuildError("fused pipeline unavailable for this model: " + why);
     }
     reset();
@@ -587,17 +594,8 @@ void Engine::validate_feeds(int n_feeds, const neng_feed* feeds, int n_steps) co
 void Engine::launch_steps(int n_steps, const float* d_feed_data, const std::vector<int>& present, float* d_ring,
                           cudaStream_t stream) {
     last_launches_ = 0;
-    std::vector<int64_t> feed_off(feeds_.size()), ring_off(probes_.size());
-    int64_t at = 0;
-    for (size_t f = 0; f < feeds_.size(); ++f) {
-        feed_off[f] = at;
-        if (present[f]) at += static_cast<int64_t>(n_steps) * feeds_[f].dim * batch_;
-    }
-    at = 0;
-    for (size_t q = 0; q < probes_.size(); ++q) {
-        ring_off[q] = at;
-        at += static_cast<int64_t>(n_steps) * probes_[q].dim * batch_;
-    }
+    std::vector<int64_t> feed_off, ring_off;
+    call_offsets(n_steps, present, &feed_off, &ring_off);
     if (fused_) {
         last_launches_ = fused_->run(n_steps, d_feed_data, feed_off.data(), present.data(), d_ring, ring_off.data(),
                                      stream);
@@ -636,6 +634,8 @@ void Engine::launch_steps(int n_steps, const float* d_feed_data, const std::vect
 void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probes_out) {
     // exec.cpp:340-366
     if (n_steps <= 0) throw RunError("n_steps must be positive");
+    if (call_steps_) throw RunError("run: a stepped call is open");
+    if (shard_count_ > 1) throw RunError("run: a sharded engine advances through neng_gpu_call_*");
     if (n_feeds < 0 || (n_feeds > 0 && !feeds)) throw InvalidArgument("bad feed array");
     validate_feeds(n_feeds, feeds, n_steps);
     const BuiltModel& m = pm_.model;
@@ -713,12 +713,12 @@ void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probe
     steps_done_ += n_steps;
 }
 
-void Engine::run_device(int n_steps, const float* const* d_feeds, float* const* d_probes, cudaStream_t stream) {
-    if (n_steps <= 0) throw RunError("n_steps must be positive");
-    if (!stream) stream = stream_;
+void Engine::device_call_args(int n_steps, const float* const* d_feeds, float* const* d_probes, const float** base_out,
+                              std::vector<int>* present_out, float** ring_out) const {
     const BuiltModel& m = pm_.model;
     // feeds: per slot pointer -> gather offsets relative to the first present block
-    std::vector<int> present(feeds_.size(), 0);
+    std::vector<int>& present = *present_out;
+    present.assign(feeds_.size(), 0);
     for (size_t f = 0; f < m.feed_slots.size(); ++f) {
         present[f] = d_feeds && d_feeds[f] ? 1 : 0;
         if (!present[f] && !m.feed_slots[f].has_default)
@@ -743,8 +743,80 @@ void Engine::run_device(int n_steps, const float* const* d_feeds, float* const* 
         if (d_probes[q] != ring + rexp) throw InvalidArgument("run_device: probe blocks must be packed in order");
         rexp += static_cast<int64_t>(n_steps) * probes_[q].dim * batch_;
     }
+    *base_out = base;
+    *ring_out = ring;
+}
+
+void Engine::call_offsets(int n_steps, const std::vector<int>& present, std::vector<int64_t>* feed_off,
+                          std::vector<int64_t>* ring_off) const {
+    feed_off->assign(feeds_.size(), 0);
+    ring_off->assign(probes_.size(), 0);
+    int64_t at = 0;
+    for (size_t f = 0; f < feeds_.size(); ++f) {
+        (*feed_off)[f] = at;
+        if (present[f]) at += static_cast<int64_t>(n_steps) * feeds_[f].dim * batch_;
+    }
+    at = 0;
+    for (size_t q = 0; q < probes_.size(); ++q) {
+        (*ring_off)[q] = at;
+        at += static_cast<int64_t>(n_steps) * probes_[q].dim * batch_;
+    }
+}
+
+void Engine::run_device(int n_steps, const float* const* d_feeds, float* const* d_probes, cudaStream_t stream) {
+    if (n_steps <= 0) throw RunError("n_steps must be positive");
+    if (call_steps_) throw RunError("run_device: a stepped call is open");
+    if (shard_count_ > 1) throw RunError("run_device: a sharded engine advances through neng_gpu_call_*");
+    if (!stream) stream = stream_;
+    const float* base = nullptr;
+    float* ring = nullptr;
+    std::vector<int> present;
+    device_call_args(n_steps, d_feeds, d_probes, &base, &present, &ring);
     launch_steps(n_steps, base, present, ring, stream);
     steps_done_ += n_steps;
+}
+
+void Engine::call_begin(int n_steps, const float* const* d_feeds, float* const* d_probes, cudaStream_t stream) {
+    if (n_steps <= 0) throw RunError("n_steps must be positive");
+    if (!fused_) throw RunError("stepped calls need the fused pipeline");
+    if (call_steps_) throw RunError("call_begin: a stepped call is already open");
+    if (!stream) stream = stream_;
+    const float* base = nullptr;
+    float* ring = nullptr;
+    std::vector<int> present;
+    device_call_args(n_steps, d_feeds, d_probes, &base, &present, &ring);
+    std::vector<int64_t> feed_off, ring_off;
+    call_offsets(n_steps, present, &feed_off, &ring_off);
+    fused_->begin(n_steps, base, feed_off.data(), present.data(), ring, ring_off.data(), stream);
+    call_steps_ = n_steps;
+    call_stream_ = stream;
+    last_launches_ = 0;
+}
+
+void Engine::call_step(int k, int flags) {
+    if (!call_steps_) throw RunError("call_step: no stepped call is open");
+    if (k < 0 || k > call_steps_ || (k == call_steps_ && !(flags & NENG_STEP_EPILOGUE)))
+        throw RunError("call_step: step " + std::to_string(k) + " is outside the call");
+    fused_->step(k, flags, call_stream_);
+    ++last_launches_;
+}
+
+void Engine::call_end() {
+    if (!call_steps_) throw RunError("call_end: no stepped call is open");
+    cuda_check(cudaStreamSynchronize(call_stream_), "stepped call");
+    steps_done_ += call_steps_;
+    call_steps_ = 0;
+}
+
+void Engine::shard_layout(int64_t* xbuf_floats, int64_t* rank_floats, float** xbuf) const {
+    if (!fused_) throw RunError("shard_layout: the engine runs the generic interpreter");
+    fused_->xhat_layout(xbuf_floats, rank_floats, xbuf);
+}
+
+void Engine::set_xhat_buffer(float* d_buf) {
+    if (!fused_) throw RunError("set_xhat_buffer: the engine runs the generic interpreter");
+    if (!d_buf) throw InvalidArgument("set_xhat_buffer: null buffer");
+    fused_->set_xhat_buffer(d_buf);
 }
 
 void Engine::synchronize() { cuda_check(cudaStreamSynchronize(stream_), "synchronize"); }

@@ -65,6 +65,14 @@ class Engine {
 
     void run(int n_steps, int n_feeds, const neng_feed* feeds, double* probes_out);
     void run_device(int n_steps, const float* const* d_feeds, float* const* d_probes, cudaStream_t stream);
+    // stepped calls (sharded runs), see neng_gpu_call_begin
+    void call_begin(int n_steps, const float* const* d_feeds, float* const* d_probes, cudaStream_t stream);
+    void call_step(int k, int flags);
+    void call_end();
+    void shard_layout(int64_t* xbuf_floats, int64_t* rank_floats, float** xbuf) const;
+    void set_xhat_buffer(float* d_buf);
+    int shard_rank() const { return shard_rank_; }
+    int shard_count() const { return shard_count_; }
     void reset();
     std::vector<double> read_signal(int sig, int batch_index) const;
     int buffer_storage(int buffer) const;
@@ -100,10 +108,17 @@ class Engine {
     void validate_feeds(int n_feeds, const neng_feed* feeds, int n_steps) const;
     void launch_steps(int n_steps, const float* d_feed_data, const std::vector<int>& present, float* d_ring,
                       cudaStream_t stream);
+    void device_call_args(int n_steps, const float* const* d_feeds, float* const* d_probes, const float** base,
+                          std::vector<int>* present, float** ring) const;
+    void call_offsets(int n_steps, const std::vector<int>& present, std::vector<int64_t>* feed_off,
+                      std::vector<int64_t>* ring_off) const;
 
     PlannedModel pm_;
     int batch_, unroll_, steps_done_ = 0;
     int device_ = 0, mode_ = NENG_MODE_GENERIC, requested_mode_ = NENG_MODE_AUTO, steps_per_launch_ = 0;
+    int shard_rank_ = 0, shard_count_ = 1;
+    int call_steps_ = 0;  // steps of the open stepped call (0: none)
+    cudaStream_t call_stream_ = nullptr;
     cudaStream_t stream_ = nullptr;
     int64_t last_launches_ = 0;
 

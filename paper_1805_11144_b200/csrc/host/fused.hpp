@@ -26,6 +26,13 @@ struct FusedPlan {
     /// Re-derive fused-private state from the arena (after reset).
     virtual void load_from_arena(cudaStream_t stream) = 0;
     virtual std::string describe() const = 0;
+    // stepped calls: per-call tables, then one launch per step (flags:
+    // NENG_STEP_FIRST_UPDATE / NENG_STEP_EPILOGUE; k == n_steps: epilogue only)
+    virtual void begin(int n_steps, const float* d_feed_data, const int64_t* feed_off, const int* present,
+                       float* d_ring, const int64_t* ring_off, cudaStream_t stream) = 0;
+    virtual void step(int k, int flags, cudaStream_t stream) = 0;
+    virtual void xhat_layout(int64_t* xbuf_floats, int64_t* rank_floats, float** xbuf) const = 0;
+    virtual void set_xhat_buffer(float* d_buf) = 0;
 };
 
 /// Returns nullptr (and a reason) when the model is not an ensemble network

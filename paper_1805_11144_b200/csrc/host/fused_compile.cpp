@@ -55,17 +55,20 @@ class FusedImpl : public FusedPlan {
   public:
     FusedProgram prog;
     int dmax = 8, grid = 1, steps_per_launch = 0;
-    DevMem d_ens, d_conns, d_incoming, d_orphans, d_values, d_probes, d_feeds, d_call, d_prof, d_work, d_xbuf, d_dq;
+    DevMem d_ens, d_conns, d_incoming, d_orphans, d_my_conns, d_values, d_probes, d_feeds, d_call, d_prof, d_work, d_xbuf;
     std::string desc;
 
-    int64_t run(int n_steps, const float* d_feed_data, const int64_t* feed_off, const int* present, float* d_ring,
-                const int64_t* ring_off, cudaStream_t stream) override {
+    FusedProgram call;  // the open call's program (begin .. step)
+
+    void begin(int n_steps, const float* d_feed_data, const int64_t* feed_off, const int* present, float* d_ring,
+               const int64_t* ring_off, cudaStream_t stream) override {
         // per-call tables: feed offsets, presence, ring offsets
         const int nf = prog.n_feeds, np = n_probe_total;
         std::vector<char> blob(static_cast<size_t>(nf) * 8 + static_cast<size_t>(np) * 8 + static_cast<size_t>(nf) * 4 + 64);
         std::memcpy(blob.data(), feed_off, nf * 8);
         std::memcpy(blob.data() + nf * 8, ring_off, np * 8);
         std::memcpy(blob.data() + nf * 8 + np * 8, present, nf * 4);
+        cuda_check(cudaStreamSynchronize(stream), "fused call tables");  // the previous call's tables are free
         d_call.ensure(blob.size());
         cuda_check(cudaMemcpyAsync(d_call.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, stream), "fused call H2D");
         FusedProgram p = prog;
@@ -75,23 +78,54 @@ class FusedImpl : public FusedPlan {
         p.feed_present = reinterpret_cast<const int32_t*>(d_call.as<char>() + nf * 8 + np * 8);
         p.ring = d_ring;
         p.call_steps = n_steps;
-        const bool profile = std::getenv("NENG_FUSED_PROFILE") != nullptr;
-        if (profile) {
+        p.prof = nullptr;
+        if (std::getenv("NENG_FUSED_PROFILE") != nullptr) {
             d_prof.ensure((FS_COUNT + 4) * 8);
             cuda_check(cudaMemsetAsync(d_prof.p, 0, (FS_COUNT + 4) * 8, stream), "profile reset");
             p.prof = d_prof.as<unsigned long long>();
         }
         d_work.ensure(16);
         p.work = d_work.as<int32_t>();
+        call = p;
+    }
+
+    void step(int k, int flags, cudaStream_t stream) override {
+        FusedProgram p = call;
+        p.first_update = (flags & NENG_STEP_FIRST_UPDATE) ? 1 : 0;
+        p.epilogue = (flags & NENG_STEP_EPILOGUE) ? 1 : 0;
+        const int k1 = k < p.call_steps ? k + 1 : k;  // k == n_steps: the epilogue of step n - 1 only
+        cuda_check(cudaMemsetAsync(d_work.p, 0, 8, stream), "fused work reset");
+        cuda_check(launch_fused(p, dmax, grid, k, k1, stream), "fused kernel launch");
+    }
+
+    void xhat_layout(int64_t* xbuf_floats, int64_t* rank_floats, float** xbuf) const override {
+        if (xbuf_floats) *xbuf_floats = static_cast<int64_t>(2) * prog.xrows * prog.batch;
+        if (rank_floats) *rank_floats = static_cast<int64_t>(xstride) * prog.batch;
+        if (xbuf) *xbuf = prog.xbuf;
+    }
+
+    void set_xhat_buffer(float* d_buf) override {
+        prog.xbuf = d_buf;
+        call.xbuf = d_buf;
+    }
+
+    int xstride = 0;  // parity-buffer rows per shard
+
+    int64_t run(int n_steps, const float* d_feed_data, const int64_t* feed_off, const int* present, float* d_ring,
+                const int64_t* ring_off, cudaStream_t stream) override {
+        begin(n_steps, d_feed_data, feed_off, present, d_ring, ring_off, stream);
         int K = steps_per_launch > 0 ? steps_per_launch : n_steps;
         int64_t launches = 0;
         for (int k = 0; k < n_steps; k += K) {
+            FusedProgram p = call;
+            p.first_update = 0;
+            p.epilogue = 1;
             cuda_check(cudaMemsetAsync(d_work.p, 0, 8, stream), "fused work reset");
             cuda_check(launch_fused(p, dmax, grid, k, std::min(n_steps, k + K), stream), "fused kernel launch");
             ++launches;
         }
         cuda_check(cudaStreamSynchronize(stream), "fused run");  // call tables are reused next call
-        if (profile) {
+        if (call.prof) {
             unsigned long long h[FS_COUNT + 4];
             cuda_check(cudaMemcpy(h, d_prof.p, sizeof h, cudaMemcpyDeviceToHost), "profile D2H");
             static const char* names[FS_COUNT] = {"deferred", "in+conn", "sweep", "queue", "fixup",
@@ -102,9 +136,6 @@ class FusedImpl : public FusedPlan {
             for (int s = 0; s < FS_COUNT; ++s)
                 std::fprintf(stderr, " %s=%.1f", names[s], h[s] / 1e3 / grid / n_steps);
             std::fprintf(stderr, " (total %.1f)\n", tot / 1e3 / grid / n_steps);
-            std::fprintf(stderr, "[fused profile] per step: doubts exit %.0f, spike out-of-range %.0f, spike window %.0f, doubt entries %.0f\n",
-                         double(h[FS_COUNT]) / n_steps, double(h[FS_COUNT + 1]) / n_steps, double(h[FS_COUNT + 2]) / n_steps,
-                         double(h[FS_COUNT + 3]) / n_steps);
         }
         return launches;
     }
@@ -343,7 +374,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         FusedProgram& p = impl->prog;
         const float dt = static_cast<float>(m.dt);
         std::vector<FEns> fe;
-        std::vector<int32_t> incoming, orphans;
+        std::vector<int32_t> incoming, orphans, my_conns;
         int nmax = 0, dmax_need = 1, pmax_floats = 0, xrows = 0;
         for (const EnsInfo& e : ens)
             dmax_need = std::max({dmax_need, m.signals[e.in].rows(), m.signals[e.xhat].rows()});
@@ -354,7 +385,27 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             while (values.size() % 4) values.push_back(0.0f);
             return static_cast<int64_t>(values.size());
         };
+        // ensemble sharding: shard s owns ensembles [lo_s, hi_s) and writes its
+        // xhat rows at s * xstride of the parity buffers (in-place all-gather)
+        const int W = eng.shard_count(), R = eng.shard_rank();
+        const int n_all = static_cast<int>(ens.size());
+        auto shard_lo = [&](int sidx) { return static_cast<int>(static_cast<int64_t>(sidx) * n_all / W); };
+        int xstride = 0;
+        for (int sidx = 0; sidx < W; ++sidx) {
+            int rows = 0;
+            for (int i = shard_lo(sidx); i < shard_lo(sidx + 1); ++i) rows += m.signals[ens[i].xhat].rows();
+            xstride = std::max(xstride, rows);
+        }
+        const int ens_lo = shard_lo(R), ens_hi = shard_lo(R + 1);
+        std::vector<int> shard_row(W, 0);
+        int ens_index = 0;
         for (EnsInfo& e : ens) {
+            const int my_shard = [&] {
+                int sidx = 0;
+                while (shard_lo(sidx + 1) <= ens_index) ++sidx;
+                return sidx;
+            }();
+            ++ens_index;
             std::stable_sort(e.incs.begin(), e.incs.end());  // plan-group order of the Copy incs
             for (size_t q = 1; q < e.incs.size(); ++q)
                 if (e.incs[q].first == e.incs[q - 1].first) fail("two increments of one input in one group");
@@ -389,8 +440,8 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             }
             x.in_init_off = push_values(m.operators[e.rin].value);
             x.xhat_init_off = push_values(m.operators[e.rx].value);
-            x.xb_row = xrows;
-            xrows += x.dx;
+            x.xb_row = my_shard * xstride + shard_row[my_shard];
+            shard_row[my_shard] += x.dx;
             const NeuronModel& nm = m.operators[e.sn].neuron;
             x.dt = dt;
             x.tau_rc = static_cast<float>(nm.tau_rc);
@@ -419,6 +470,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             dmax_need = std::max({dmax_need, x.d, x.dx});
             fe.push_back(x);
         }
+        xrows = W * xstride;
         std::vector<FConn> fc;
         for (const ConnInfo& c : conns) {
             FConn x{};
@@ -431,6 +483,8 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             x.src_feed = -1;
             x.src_xb = ens_of_xhat.count(c.src) ? fe[ens_of_xhat.at(c.src)].xb_row : -1;
             if (c.dst_ens < 0) orphans.push_back(static_cast<int32_t>(fc.size()));
+            if ((c.dst_ens < 0 && R == 0) || (c.dst_ens >= ens_lo && c.dst_ens < ens_hi))
+                my_conns.push_back(static_cast<int32_t>(fc.size()));
             if (slot_of_sig.count(c.src)) {
                 x.src_feed = slot_of_sig[c.src];
                 if (m.feed_slots[x.src_feed].dim != x.ds) fail("feed slot dim differs from its signal");
@@ -468,7 +522,10 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
                 pr.xb_row = ens_of_xhat.count(s) ? fe[ens_of_xhat.at(s)].xb_row : -1;
                 if (pr.feed_slot >= 0 && m.feed_slots[pr.feed_slot].dim != pr.dim)
                     fail("feed slot dim differs from its signal");
-                fp.push_back(pr);
+                // captured by the shard that produces the value (fed nodes: shard 0)
+                const bool mine = ens_of_xhat.count(s) ? (ens_of_xhat.at(s) >= ens_lo && ens_of_xhat.at(s) < ens_hi)
+                                                       : R == 0;
+                if (mine) fp.push_back(pr);
             } else if (conn_of_filt.count(s)) {
                 FConn& x = fc[conn_of_filt[s]];
                 if (x.probe_filt >= 0) fail("two probes on one filtered value");
@@ -517,7 +574,14 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         p.orphans = impl->d_orphans.as<int32_t>();
         p.xbuf = impl->d_xbuf.as<float>();
         p.xrows = xrows;
-        p.n_orphans = static_cast<int32_t>(orphans.size());
+        p.n_orphans = R == 0 ? static_cast<int32_t>(orphans.size()) : 0;
+        upload(impl->d_my_conns, my_conns.data(), my_conns.size() * sizeof(int32_t));
+        p.my_conns = impl->d_my_conns.as<int32_t>();
+        p.n_my_conns = static_cast<int32_t>(my_conns.size());
+        p.ens_lo = ens_lo;
+        p.ens_hi = ens_hi;
+        impl->xstride = xstride;
+        if (R != 0) p.time_probe_step = p.time_probe_time = -1;  // the clock's captures live on shard 0
         p.probes = impl->d_probes.as<FProbe>();
         p.feeds = impl->d_feeds.as<FFeed>();
         p.n_ens = static_cast<int32_t>(fe.size());
@@ -558,7 +622,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         impl->dmax = fused_dmax_for(dmax_need);
         int cap = fused_max_grid(p, impl->dmax, eng.device());
         if (cap <= 0) fail("fused kernel does not fit on the device");
-        int64_t work = std::max<int64_t>(static_cast<int64_t>(p.n_ens) * p.groups,
+        int64_t work = std::max<int64_t>(static_cast<int64_t>(ens_hi - ens_lo) * p.groups,
                                          (static_cast<int64_t>(p.n_conn) * B + 255) / 256);
         impl->grid = static_cast<int>(std::min<int64_t>(cap, std::max<int64_t>(1, work)));
 

@@ -399,12 +399,13 @@ __device__ void grid_step_work(const FusedProgram& p, int kk, bool all_conns, bo
     const int B = batch_of<BT>(p);
     const int64_t gthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
     const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int nc = all_conns ? p.n_conn : p.n_orphans;
+    const int nc = all_conns ? p.n_my_conns : p.n_orphans;
+    const int* list = all_conns ? p.my_conns : p.orphans;
     const int64_t items = static_cast<int64_t>(nc) * B;
     for (int64_t it = gtid; it < items; it += gthreads) {
         const int q = static_cast<int>(it / B);
         const int b = static_cast<int>(it - static_cast<int64_t>(q) * B);
-        const int c = all_conns ? q : __ldg(p.orphans + q);
+        const int c = __ldg(list + q);
         float f[DMAX];
         conn_rows<DMAX, BT>(p, p.conns[c], kk, b, 0, p.conns[c].dd, true, last, f);
     }
@@ -461,8 +462,9 @@ template <int DMAX, int BT, bool PROF>
 __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bool last, const Smem& S,
                          uint32_t parity, Ticker<PROF>& tk) {
     const int B = batch_of<BT>(p);
-    const int ei = u / p.groups;
-    const int g = u - ei * p.groups;
+    const int ul = u / p.groups;
+    const int g = u - ul * p.groups;
+    const int ei = p.ens_lo + ul;
     const FEns e = p.ens[ei];  // a private copy: fields stay in registers across the arena stores
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tslot = warp / p.slices, slice = warp - tslot * p.slices;
@@ -776,7 +778,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_run_kernel(const __grid_con
     __syncthreads();
     uint32_t parity = 0;
     const int B = batch_of<BT>(p);
-    const int units = p.n_ens * p.groups;
+    const int units = (p.ens_hi - p.ens_lo) * p.groups;
     const int64_t gthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
     const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     Ticker<PROF> tk;
@@ -798,7 +800,8 @@ __global__ void __launch_bounds__(kThreads, 2) fused_run_kernel(const __grid_con
                 p.arena[fd.base + d * (fd.copies > 1 ? B : 1) + bb] = src[d * B + bb];
             }
         }
-        if (k > k_begin) grid_step_work<DMAX, BT>(p, k - 1, false, false);
+        const bool upd = k > k_begin || p.first_update;
+        if (upd) grid_step_work<DMAX, BT>(p, k - 1, false, false);
         tk.tick(FS_DEFER);
         int* work = p.work + (k & 1);
         for (;;) {
@@ -807,7 +810,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_run_kernel(const __grid_con
             const int u = *S.cur;
             __syncthreads();  // every thread has read cur before thread 0 claims again
             if (u >= units) break;  // uniform
-            run_unit<DMAX, BT, PROF>(p, u, k, k > k_begin, last, S, parity, tk);
+            run_unit<DMAX, BT, PROF>(p, u, k, upd, last, S, parity, tk);
             parity ^= 1u;
             __syncthreads();  // staging buffers, words and queues are reused by the next unit
         }
@@ -815,7 +818,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_run_kernel(const __grid_con
         tk.tick(FS_BAR);
     }
     // epilogue: connection updates, captures and clock of the launch's last step
-    grid_step_work<DMAX, BT>(p, k_end - 1, true, k_end - 1 == p.call_steps - 1);
+    if (p.epilogue) grid_step_work<DMAX, BT>(p, k_end - 1, true, k_end - 1 == p.call_steps - 1);
     tk.tick(FS_EPI);
     tk.flush(p.prof);
 }

@@ -17,6 +17,11 @@
 // The update of step k-1 for connections without a destination ensemble, the
 // probe captures of step k-1 and the clock run at the start of step k; the
 // launch's last step is completed by an epilogue after a final barrier.
+//
+// Ensemble sharding (one engine per GPU): a shard owns a contiguous range of
+// ensembles and the connections into them; its units write xhat rows
+// [rank * stride, ...) of the parity buffer, which the host all-gathers
+// between per-step launches (first_update / epilogue select the pieces).
 // J, out, in, acc and filt reach the arena on a call's last step only, so the
 // arena holds the reference's full state at every call boundary.
 #pragma once
@@ -76,11 +81,13 @@ struct FusedProgram {
     const FEns* ens = nullptr;
     const FConn* conns = nullptr;
     const int32_t* incoming = nullptr;  // per ensemble, plan order: connection indices
-    const int32_t* orphans = nullptr;   // connections with no destination ensemble
+    const int32_t* orphans = nullptr;   // connections with no destination ensemble (updated by shard 0)
+    const int32_t* my_conns = nullptr;  // connections this shard updates: into its ensembles (+ orphans on shard 0)
     const FProbe* probes = nullptr;
     const FFeed* feeds = nullptr;
     float* xbuf = nullptr;  // two parity buffers of xrows rows x B
-    int32_t n_ens = 0, n_conn = 0, n_orphans = 0, n_probes = 0, n_feeds = 0;
+    int32_t n_ens = 0, n_conn = 0, n_orphans = 0, n_probes = 0, n_feeds = 0, n_my_conns = 0;
+    int32_t ens_lo = 0, ens_hi = 0;  // this shard's ensembles (all of them unsharded)
     int32_t xrows = 0;
     int32_t batch = 1, btiles = 1, nmax = 0;
     int32_t tu = 8, slices = 1, groups = 1;  // tiles per unit, warps per tile, units per ensemble
@@ -97,6 +104,8 @@ struct FusedProgram {
     float* ring = nullptr;
     const int64_t* ring_off = nullptr;  // per probe
     int32_t call_steps = 0;
+    int32_t first_update = 0;  // apply the step k_begin-1 connection updates at k_begin (stepped / sharded runs)
+    int32_t epilogue = 1;      // complete the launch's last step (connection updates, captures, clock)
     // optional section timers (NENG_FUSED_PROFILE=1): per-CTA ns summed over CTAs
     unsigned long long* prof = nullptr;
     int32_t* work = nullptr;  // two unit counters (step parity), zero at launch

@@ -19,6 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libneng_gpu.so")
 
 MODE_AUTO, MODE_GENERIC, MODE_FUSED = 0, 1, 2
+STEP_FIRST_UPDATE, STEP_EPILOGUE = 1, 2
 
 _lib = None
 
@@ -38,6 +39,11 @@ def lib():
         L.neng_gpu_run.argtypes = [P, C.c_int32, C.c_int32, C.POINTER(_abi.neng_feed), C.POINTER(C.c_double)]
         L.neng_gpu_run_device.argtypes = [P, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), P]
         L.neng_gpu_synchronize.argtypes = [P]
+        L.neng_gpu_call_begin.argtypes = [P, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), P]
+        L.neng_gpu_call_step.argtypes = [P, C.c_int32, C.c_int32]
+        L.neng_gpu_call_end.argtypes = [P]
+        L.neng_gpu_shard_layout.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_void_p)]
+        L.neng_gpu_set_xhat_buffer.argtypes = [P, P]
         L.neng_gpu_reset.argtypes = [P]
         L.neng_gpu_read_signal.argtypes = [P, C.c_int32, C.c_int32, C.POINTER(C.c_double), C.c_int64,
                                            C.POINTER(C.c_int64)]
@@ -65,7 +71,7 @@ class GpuEngine:
     """
 
     def __init__(self, planned: ir.PlannedModel, batch: int = 1, unroll: int = 1, *, device: int = 0,
-                 mode: int = MODE_AUTO, steps_per_launch: int = 0):
+                 mode: int = MODE_AUTO, steps_per_launch: int = 0, shard: Optional[tuple] = None):
         L = lib()
         self._planned = planned
         self.model = planned.model
@@ -73,6 +79,8 @@ class GpuEngine:
         view = _abi.planned_model_view(planned, m)
         cfg = _abi.neng_device_cfg()
         cfg.device, cfg.mode, cfg.steps_per_launch = device, mode, steps_per_launch
+        if shard is not None:  # (rank, count): ensemble sharding, see paper_1805_11144_b200.shard
+            cfg.shard_rank, cfg.shard_count = int(shard[0]), int(shard[1])
         h = C.c_void_p()
         st = L.neng_gpu_create(C.byref(view), batch, unroll, C.byref(cfg), C.byref(h))
         if st:
@@ -106,6 +114,30 @@ class GpuEngine:
         npb = len(self.model.probes)
         pp = (C.c_void_p * max(npb, 1))(*[C.c_void_p(p) if p else None for p in (probe_ptrs or [None] * npb)])
         self._check(lib().neng_gpu_run_device(self._h, n_steps, fp, pp, C.c_void_p(stream) if stream else None))
+
+    # -- stepped calls (ensemble sharding) -------------------------------------
+    def _ptrs(self, ptrs, n):
+        return (C.c_void_p * max(n, 1))(*[C.c_void_p(q) if q else None for q in (ptrs or [None] * n)])
+
+    def call_begin(self, n_steps: int, feed_ptrs, probe_ptrs, stream: int = 0):
+        fp = self._ptrs(feed_ptrs, len(self.model.feed_slots))
+        pp = self._ptrs(probe_ptrs, len(self.model.probes))
+        self._check(lib().neng_gpu_call_begin(self._h, n_steps, fp, pp, C.c_void_p(stream) if stream else None))
+
+    def call_step(self, k: int, flags: int = 0):
+        self._check(lib().neng_gpu_call_step(self._h, k, flags))
+
+    def call_end(self):
+        self._check(lib().neng_gpu_call_end(self._h))
+
+    def shard_layout(self):
+        """(xbuf_floats, rank_floats, device pointer of the xhat parity buffers)."""
+        a, b, q = C.c_int64(), C.c_int64(), C.c_void_p()
+        self._check(lib().neng_gpu_shard_layout(self._h, C.byref(a), C.byref(b), C.byref(q)))
+        return a.value, b.value, q.value
+
+    def set_xhat_buffer(self, ptr: int):
+        self._check(lib().neng_gpu_set_xhat_buffer(self._h, C.c_void_p(ptr)))
 
     def synchronize(self):
         self._check(lib().neng_gpu_synchronize(self._h))

@@ -89,3 +89,95 @@ def test_config4_full_batch_sampled_rows_bit_exact():
         for s in pm.model.signals[::97]:
             assert np.array_equal(gpu.read_signal(s.id, b).view(np.uint64), solo.read_signal(s.id, 0).view(np.uint64)), \
                 f"row {b} signal {s.label}"
+
+
+def _device_feeds(w, steps, dev):
+    """w.feeds ([batch][steps][dim] f64 per node) as one packed [slot][step][dim][B] f32 block."""
+    import torch
+    blocks = []
+    for fs in w.model.feed_slots:
+        f = w.feeds[fs.node_id][:, :steps, :]
+        blocks.append(torch.as_tensor(np.ascontiguousarray(f.transpose(1, 2, 0)), dtype=torch.float32).reshape(-1))
+    flat = torch.cat(blocks).to(dev) if blocks else torch.zeros(1, device=dev)
+    ptrs, at = [], 0
+    for fs in w.model.feed_slots:
+        ptrs.append(flat.data_ptr() + 4 * at)
+        at += steps * fs.dim * w.batch
+    return flat, ptrs
+
+
+def _device_ring(model, steps, batch, dev):
+    import torch
+    dims = [model.signals[p.signal].size() for p in model.probes]
+    ring = torch.full((max(sum(dims) * steps * batch, 1),), float("nan"), device=dev)
+    ptrs, offs, at = [], [], 0
+    for d in dims:
+        ptrs.append(ring.data_ptr() + 4 * at)
+        offs.append((at, d * steps * batch))
+        at += d * steps * batch
+    return ring, ptrs, offs
+
+
+def test_two_ensemble_shards_match_the_unsharded_engine():
+    # two shards of one network driven on one GPU (their launches never wait on each other;
+    # the "all-gather" is a copy of each shard's xhat rows into the other's parity buffer)
+    import torch
+
+    dev = torch.device("cuda", 0)
+    # probes on every ensemble's xhat, so both shards own some
+    w = networks.random_network(11, n_ens=10, n=96, d=6, k_out=3, n_inputs=3, batch=64, steps=16, probes=10)
+    pm = passes.run_passes(w.model)
+    n, B = w.steps, w.batch
+    ts = torch.cuda.Stream(dev)  # a real stream: the engine, the copies and the feeds must be ordered
+    with torch.cuda.stream(ts):
+        _two_shards_on_one_stream(pm, w, n, B, dev, ts.cuda_stream)
+
+
+def _two_shards_on_one_stream(pm, w, n, B, dev, stream):
+    import torch
+    from paper_1805_11144_b200.engine import STEP_EPILOGUE, STEP_FIRST_UPDATE
+    from paper_1805_11144_b200.shard import attach_xhat_buffer
+    feeds, fptrs = _device_feeds(w, n, dev)
+
+    whole = GpuEngine(pm, B)
+    ring_w, rptrs_w, offs = _device_ring(pm.model, n, B, dev)
+    whole.run_device(n, fptrs, rptrs_w, stream)
+
+    shards = [GpuEngine(pm, B, shard=(r, 2)) for r in range(2)]
+    xb = [attach_xhat_buffer(s, dev) for s in shards]
+    rings = [_device_ring(pm.model, n, B, dev) for _ in shards]
+    for s, (ring, rptrs, _) in zip(shards, rings):
+        s.call_begin(n, fptrs, rptrs, stream)
+    rf = xb[0][1]
+    half = xb[0][0].numel() // 2
+    for k in range(n):
+        for s in shards:
+            s.call_step(k, STEP_FIRST_UPDATE if k else 0)
+        h = (k & 1) * half
+        for r in range(2):  # shard r's rows into the other shard's buffer
+            src = xb[r][0][h + r * rf:h + (r + 1) * rf]
+            xb[1 - r][0][h + r * rf:h + (r + 1) * rf].copy_(src)
+    for s in shards:
+        s.call_step(n, STEP_EPILOGUE)
+    for s in shards:
+        s.call_end()
+    torch.cuda.synchronize(dev)
+
+    # every probe is produced by exactly one shard: its trace equals the unsharded one
+    owned = 0
+    for (at, cnt) in offs:
+        ref = ring_w[at:at + cnt].cpu().numpy().view(np.uint32)
+        got = [rg[0][at:at + cnt].cpu().numpy() for rg in rings]
+        mine = [g for g in got if not np.isnan(g).all()]
+        assert len(mine) == 1
+        assert np.array_equal(mine[0].view(np.uint32), ref)
+        owned += 1
+    assert owned == len(pm.model.probes)
+    # neuron state of each shard's ensembles equals the unsharded engine's
+    sig = {s.label: s.id for s in pm.model.signals}
+    for e in range(10):
+        owner = shards[0 if e < 5 else 1]
+        for name in (f"ens{e}.voltage", f"ens{e}.refractory"):
+            for b in (0, B - 1):
+                assert np.array_equal(owner.read_signal(sig[name], b).view(np.uint64),
+                                      whole.read_signal(sig[name], b).view(np.uint64)), (name, b)
