@@ -163,8 +163,15 @@ typedef struct neng_device_cfg {
      * ranges and the connections into them; the caller all-gathers the xhat
      * parity buffer between per-step calls (neng_gpu_call_*). */
     int32_t shard_rank, shard_count;
-    int32_t reserved[3];
+    /* NENG_PRECISION_*: STRICT_FP32 (default) reproduces EngineCore<float> bit for
+     * bit; TF32 runs dense DotInc groups (shared 2-D weights >= 32x32, per-batch
+     * input and output, batch >= 32) as tensor-core GEMMs with fp32 accumulation
+     * (TF32 products: a stated tolerance instead of bit-exact results). */
+    int32_t precision;
+    int32_t reserved[2];
 } neng_device_cfg;
+
+enum { NENG_PRECISION_STRICT_FP32 = 0, NENG_PRECISION_TF32 = 1 };
 
 typedef struct neng_engine neng_engine;
 

@@ -69,7 +69,8 @@ class neng_feed(C.Structure):
 
 class neng_device_cfg(C.Structure):
     _fields_ = [("device", C.c_int32), ("mode", C.c_int32), ("steps_per_launch", C.c_int32),
-                ("shard_rank", C.c_int32), ("shard_count", C.c_int32), ("reserved", C.c_int32 * 3)]
+                ("shard_rank", C.c_int32), ("shard_count", C.c_int32), ("precision", C.c_int32),
+                ("reserved", C.c_int32 * 2)]
 
 
 STATUS_EXC = {1: ir.StructuralError, 2: ir.BuildError, 3: ir.RunError, 4: ir.CudaError,

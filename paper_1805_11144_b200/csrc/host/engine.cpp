@@ -15,6 +15,8 @@
 #include <thread>
 #include <unordered_map>
 
+#include <cublas_v2.h>
+
 #include "fused.hpp"
 
 namespace nengb {
@@ -281,7 +283,10 @@ Engine::Engine(PlannedModel planned, int batch, int unroll, const neng_device_cf
         steps_per_launch_ = cfg->steps_per_launch;
         shard_rank_ = cfg->shard_rank;
         shard_count_ = cfg->shard_count > 0 ? cfg->shard_count : 1;
+        precision_ = cfg->precision;
     }
+    if (precision_ != NENG_PRECISION_STRICT_FP32 && precision_ != NENG_PRECISION_TF32)
+        throw BuildError("unknown precision mode " + std::to_string(precision_));
     if (shard_count_ < 1 || shard_rank_ < 0 || shard_rank_ >= shard_count_)
         throw BuildError("shard rank " + std::to_string(shard_rank_) + " is outside [0, " +
                          std::to_string(shard_count_) + ")");
@@ -294,6 +299,7 @@ Engine::Engine(PlannedModel planned, int batch, int unroll, const neng_device_cf
 
 Engine::~Engine() {
     fused_.reset();
+    if (cublas_) cublasDestroy(static_cast<cublasHandle_t>(cublas_));
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -495,6 +501,22 @@ void Engine::compile_generic() {
         g.n_members = static_cast<int32_t>(members.size()) - g.member_begin;
         g.n_tiles = static_cast<int32_t>(tiles.size()) - g.tile_begin;
         g.flags |= GF_BARRIER;
+        if (precision_ == NENG_PRECISION_TF32 && first.kind == OpKind::DotInc && batch_ >= 32 &&
+            (g.flags & GF_PER_BATCH) && !(g.flags & (GF_SERIAL_ALL | GF_SERIAL_B))) {
+            // C[M][B] += A[M][K] X[K][B]: shared row-major weights, per-batch input and output
+            TcGroup tg;
+            tg.group = static_cast<int>(groups.size());
+            bool ok = true;
+            for (int mi = g.member_begin; mi < static_cast<int>(members.size()) && ok; ++mi) {
+                const DMember& dm = members[mi];
+                const DArg &A = dm.a[0], &X = dm.a[1], &Y = dm.a[2];
+                const int64_t M = Y.elems, K = X.elems;
+                ok = A.bs == 0 && A.es == 1 && A.elems == M * K && X.es == batch_ && X.bs == 1 && Y.es == batch_ &&
+                     Y.bs == 1 && M >= 32 && K >= 32;
+                if (ok) tg.gemms.push_back({A.base, X.base, Y.base, static_cast<int>(M), static_cast<int>(K)});
+            }
+            if (ok) tc_groups_.push_back(std::move(tg));
+        }
         if (!(g.flags & (GF_SERIAL_ALL | GF_SERIAL_B))) max_tiles = std::max(max_tiles, g.n_tiles);
         groups.push_back(g);
     }
@@ -622,13 +644,57 @@ void Engine::launch_steps(int n_steps, const float* d_feed_data, const std::vect
     p.feed_data = d_feed_data;
     p.ring = d_ring;
     p.call_steps = n_steps;
-    int K = steps_per_launch_ > 0 ? steps_per_launch_ : n_steps;
-    for (int k = 0; k < n_steps; k += K) {
-        cuda_check(launch_generic(p, grid_, k, std::min(n_steps, k + K), 0, stream), "generic kernel launch");
-        ++last_launches_;
+    if (!tc_groups_.empty()) {
+        // per step: interpreter segments between the tensor-core groups (feeds with the
+        // first segment, probe captures with the last), the GEMMs in stream order between
+        for (int k = 0; k < n_steps; ++k) {
+            int seg = 0;
+            for (const TcGroup& tg : tc_groups_) {
+                if (tg.group > seg || seg == 0) {
+                    GenericProgram q = p;
+                    q.g_begin = seg;
+                    q.g_end = tg.group;
+                    cuda_check(launch_generic(q, grid_, k, k + 1, 0, stream), "generic kernel launch");
+                    ++last_launches_;
+                }
+                run_tc_gemms(tg, stream);
+                last_launches_ += static_cast<int64_t>(tg.gemms.size());
+                seg = tg.group + 1;
+            }
+            GenericProgram q = p;
+            q.g_begin = seg;
+            q.g_end = -1;
+            cuda_check(launch_generic(q, grid_, k, k + 1, 0, stream), "generic kernel launch");
+            ++last_launches_;
+        }
+    } else {
+        int K = steps_per_launch_ > 0 ? steps_per_launch_ : n_steps;
+        for (int k = 0; k < n_steps; k += K) {
+            cuda_check(launch_generic(p, grid_, k, std::min(n_steps, k + K), 0, stream), "generic kernel launch");
+            ++last_launches_;
+        }
     }
     // the descriptor upload must finish before the host vectors change again
     cuda_check(cudaStreamSynchronize(stream), "generic run");
+}
+
+void Engine::run_tc_gemms(const TcGroup& tg, cudaStream_t stream) {
+    if (!cublas_) {
+        cublasHandle_t h = nullptr;
+        if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasCreate failed");
+        cublas_ = h;
+    }
+    cublasHandle_t h = static_cast<cublasHandle_t>(cublas_);
+    if (cublasSetStream(h, stream) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream failed");
+    const float one = 1.0f;
+    float* A = arena_.as<float>();
+    for (const TcGemm& g : tg.gemms) {
+        // row-major C[M][B] += A[M][K] X[K][B]  ==  column-major C^T (B x M) += X^T (B x K) A^T (K x M)
+        cublasStatus_t st = cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, batch_, g.m, g.k, &one, A + g.x, CUDA_R_32F,
+                                         batch_, A + g.a, CUDA_R_32F, g.k, &one, A + g.y, CUDA_R_32F, batch_,
+                                         CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT);
+        if (st != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasGemmEx failed: " + std::to_string(static_cast<int>(st)));
+    }
 }
 
 void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probes_out) {

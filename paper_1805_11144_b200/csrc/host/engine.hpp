@@ -117,6 +117,19 @@ class Engine {
     int batch_, unroll_, steps_done_ = 0;
     int device_ = 0, mode_ = NENG_MODE_GENERIC, requested_mode_ = NENG_MODE_AUTO, steps_per_launch_ = 0;
     int shard_rank_ = 0, shard_count_ = 1;
+    int precision_ = NENG_PRECISION_STRICT_FP32;
+    // dense DotInc groups run as tensor-core GEMMs (precision_ == TF32)
+    struct TcGemm {
+        int64_t a, x, y;  // arena offsets: A [M][K] shared, X [K][B], Y [M][B]
+        int m, k;
+    };
+    struct TcGroup {
+        int group;
+        std::vector<TcGemm> gemms;
+    };
+    std::vector<TcGroup> tc_groups_;
+    void* cublas_ = nullptr;  // cublasHandle_t
+    void run_tc_gemms(const TcGroup& g, cudaStream_t stream);
     int call_steps_ = 0;  // steps of the open stepped call (0: none)
     cudaStream_t call_stream_ = nullptr;
     cudaStream_t stream_ = nullptr;

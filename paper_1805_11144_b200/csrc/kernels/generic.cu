@@ -190,7 +190,8 @@ __global__ void __launch_bounds__(kTile) generic_run_kernel(GenericProgram p, in
     for (int k = k_begin; k < k_end; ++k) {
         const int ks = k - call_k0;  // step index within this run() call
         // write_feeds (exec.cpp:313-326): per-batch slots take row b, shared slots row 0
-        if (p.any_feed) {
+        const int g_end = p.g_end < 0 ? p.n_groups : p.g_end;
+        if (p.any_feed && p.g_begin == 0) {
             for (int f = 0; f < p.n_feeds; ++f) {
                 const DFeed& fd = p.feeds[f];
                 if (!fd.present) continue;
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(kTile) generic_run_kernel(GenericProgram p, in
             }
             grid_sync(grid);
         }
-        for (int gi = 0; gi < p.n_groups; ++gi) {
+        for (int gi = p.g_begin; gi < g_end; ++gi) {
             const DGroup g = p.groups[gi];
             if (g.flags & GF_SERIAL_ALL) {
                 if (blockIdx.x == 0 && threadIdx.x == 0)
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(kTile) generic_run_kernel(GenericProgram p, in
             if (g.flags & GF_BARRIER) grid_sync(grid);
         }
         // capture_probes (exec.cpp:328-338): shared probes read copy 0
-        if (p.n_probes) {
+        if (p.n_probes && g_end == p.n_groups) {
             for (int q = 0; q < p.n_probes; ++q) {
                 const DProbe& pr = p.probes[q];
                 const int64_t n = static_cast<int64_t>(pr.dim) * B;

@@ -103,6 +103,8 @@ struct GenericProgram {
     const DFeed* feeds = nullptr;
     const DProbe* probes = nullptr;
     int32_t n_groups = 0, n_feeds = 0, n_probes = 0, batch = 1;
+    int32_t g_begin = 0, g_end = -1;  // plan groups this launch runs (-1: to the end); feeds with
+                                      // the first group, probe captures with the last
     int32_t any_feed = 0;
     LibmTables libm;
     // per call

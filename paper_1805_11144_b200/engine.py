@@ -19,6 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libneng_gpu.so")
 
 MODE_AUTO, MODE_GENERIC, MODE_FUSED = 0, 1, 2
+PRECISION_STRICT_FP32, PRECISION_TF32 = 0, 1
 STEP_FIRST_UPDATE, STEP_EPILOGUE = 1, 2
 
 _lib = None
@@ -71,7 +72,8 @@ class GpuEngine:
     """
 
     def __init__(self, planned: ir.PlannedModel, batch: int = 1, unroll: int = 1, *, device: int = 0,
-                 mode: int = MODE_AUTO, steps_per_launch: int = 0, shard: Optional[tuple] = None):
+                 mode: int = MODE_AUTO, steps_per_launch: int = 0, shard: Optional[tuple] = None,
+                 precision: int = PRECISION_STRICT_FP32):
         L = lib()
         self._planned = planned
         self.model = planned.model
@@ -79,6 +81,7 @@ class GpuEngine:
         view = _abi.planned_model_view(planned, m)
         cfg = _abi.neng_device_cfg()
         cfg.device, cfg.mode, cfg.steps_per_launch = device, mode, steps_per_launch
+        cfg.precision = precision  # PRECISION_TF32: dense DotInc on tensor cores (stated tolerance)
         if shard is not None:  # (rank, count): ensemble sharding, see paper_1805_11144_b200.shard
             cfg.shard_rank, cfg.shard_count = int(shard[0]), int(shard[1])
         h = C.c_void_p()

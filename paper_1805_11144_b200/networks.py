@@ -300,10 +300,13 @@ def config4(seed: int = 1, steps: int = 500, batch: int = 256) -> Workload:
     return random_network(seed, 2048, 512, 8, 8, 256, batch, steps, name="config4_random_2048x512")
 
 
-def config3(seed: int = 1, steps: int = 100, batch: int = 512) -> Workload:
-    """Spiking MLP 784-1024-1024-10: LIF hidden layers (amplitude 0.01, gain 1,
-    bias 0), Glorot-uniform weights, lowpass 0.005 between layers, constant
-    U[0,1] inputs fed per sample."""
+def config3(seed: int = 1, steps: int = 100, batch: int = 512, gain: float = 4.0) -> Workload:
+    """Spiking MLP 784-1024-1024-10: LIF hidden layers (amplitude 0.01, bias 0),
+    Glorot-uniform weights, lowpass 0.005 between layers, constant U[0,1]
+    inputs fed per sample.  The RectifiedLinear->LIF conversion scales each
+    hidden layer's input weights by `gain` (4: with gain 1 the Glorot-scaled
+    currents stay below the LIF threshold in the second layer and the output
+    is silent)."""
     nb = NetBuilder(seed)
     rng = np.random.default_rng(derive_seed(seed, 3) % (2 ** 63))
     sizes = [784, 1024, 1024, 10]
@@ -326,10 +329,10 @@ def config3(seed: int = 1, steps: int = 100, batch: int = 512) -> Workload:
         r = m.add_signal(f"l{li}.refractory", [n], minibatched=True)
         m.operators.append(Operator.reset(m.next_op(), m.full(j), np.zeros(n)))
         if li == 1:
-            W = m.add_signal("W1", [n, sizes[0]], glorot(n, sizes[0]).ravel(), constant=True, trainable=True)
+            W = m.add_signal("W1", [n, sizes[0]], (gain * glorot(n, sizes[0])).ravel(), constant=True, trainable=True)
             m.operators.append(Operator.dot_inc(m.next_op(), m.full(W), m.full(src), m.full(j)))
         else:
-            nb.connect(src, j, glorot(n, sizes[li - 1]), synapse=0.005)
+            nb.connect(src, j, gain * glorot(n, sizes[li - 1]), synapse=0.005)
         m.operators.append(Operator.sim_neurons(m.next_op(), lif, m.full(j), m.full(out), [m.full(v), m.full(r)]))
         h.append(out)
         src = out

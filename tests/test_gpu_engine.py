@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from oracle import refapi
-from paper_1805_11144_b200 import ir
+from paper_1805_11144_b200 import ir, networks, passes
 from paper_1805_11144_b200.engine import MODE_GENERIC, GpuEngine
 from paper_1805_11144_b200.ir import Operator, SignalRef
 from tests.support.models import (assert_bitexact, batch_slice, chain_model, concat_steps, learning_model,
@@ -244,3 +244,26 @@ def test_committed_golden_fixtures(name):
     planned, batch, steps, feeds, probes = load_case(os.path.join(os.path.dirname(__file__), "golden", f"{name}.npz"))
     for mode in (MODE_GENERIC, 0):
         assert_bitexact(GpuEngine(planned, batch, mode=mode).run(steps, feeds), probes, f"{name} mode {mode}")
+
+
+def test_config3_strict_matches_reference_and_tf32_within_tolerance():
+    # BASELINE config 3 (spiking MLP 784-1024-1024-10), batch and steps reduced for the CPU reference.
+    # Strict fp32 is bit-exact; the TF32 tensor-core path (dense DotInc as cuBLAS TF32 GEMMs with fp32
+    # accumulation) is held to the stated tolerance: the rate-coded output (mean of the filtered output
+    # over the second half of the run, per sample) within 10% relative L2 of the strict result.
+    from paper_1805_11144_b200.engine import PRECISION_TF32
+    w = networks.config3(steps=40, batch=32)
+    pm = passes.run_passes(w.model)
+    ref = refapi.RefEngine(pm, w.batch).run(w.steps, w.feeds)
+    strict = GpuEngine(pm, w.batch)
+    out = strict.run(w.steps, w.feeds)
+    assert_bitexact(out, ref, "config3 strict")
+    tc = GpuEngine(pm, w.batch, precision=PRECISION_TF32)
+    fast = tc.run(w.steps, w.feeds)
+    assert tc.last_launch_count() > w.steps  # the dense layers left the interpreter
+    (k,) = list(ref)
+    a = ref[k][:, w.steps // 2:].mean(axis=1)
+    b = fast[k][:, w.steps // 2:].mean(axis=1)
+    assert np.abs(a).max() > 0.1  # the network is active
+    rel = np.linalg.norm(a - b) / np.linalg.norm(a)
+    assert rel < 0.10, rel
