@@ -720,18 +720,36 @@ void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probe
     }
     feed_stage_.ensure(static_cast<size_t>(std::max<int64_t>(feed_floats, 1)) * sizeof(float));
     float* stage = feed_stage_.as<float>();
-    int64_t at = 0;
-    for (size_t f = 0; f < feeds_.size(); ++f) {
-        if (!present[f]) continue;
-        const neng_feed* t = src[f];
-        const int dim = feeds_[f].dim;
-        for (int s = 0; s < n_steps; ++s)
-            for (int d = 0; d < dim; ++d) {
-                float* row = stage + at + (static_cast<int64_t>(s) * dim + d) * B;
-                for (int b = 0; b < B; ++b)
-                    row[b] = static_cast<float>(t->data[(static_cast<int64_t>(b) * t->steps + s) * t->dim + d]);
+    {
+        // transpose + narrow on the host cores: slot blocks are independent
+        std::vector<std::pair<size_t, int64_t>> jobs;  // (slot, offset in the stage)
+        int64_t at = 0;
+        for (size_t f = 0; f < feeds_.size(); ++f) {
+            if (!present[f]) continue;
+            jobs.emplace_back(f, at);
+            at += static_cast<int64_t>(n_steps) * feeds_[f].dim * B;
+        }
+        auto work = [&](size_t j0, size_t j1) {
+            for (size_t j = j0; j < j1; ++j) {
+                const auto [f, off] = jobs[j];
+                const neng_feed* t = src[f];
+                const int dim = feeds_[f].dim;
+                for (int s = 0; s < n_steps; ++s)
+                    for (int d = 0; d < dim; ++d) {
+                        float* row = stage + off + (static_cast<int64_t>(s) * dim + d) * B;
+                        for (int b = 0; b < B; ++b)
+                            row[b] = static_cast<float>(t->data[(static_cast<int64_t>(b) * t->steps + s) * t->dim + d]);
+                    }
             }
-        at += static_cast<int64_t>(n_steps) * dim * B;
+        };
+        const size_t nt = std::min<size_t>(jobs.size(), std::max(1u, std::thread::hardware_concurrency()));
+        if (nt <= 1 || feed_floats < (int64_t{1} << 20)) {
+            work(0, jobs.size());
+        } else {
+            std::vector<std::thread> pool;
+            for (size_t t = 0; t < nt; ++t) pool.emplace_back(work, jobs.size() * t / nt, jobs.size() * (t + 1) / nt);
+            for (auto& th : pool) th.join();
+        }
     }
     feed_buf_.ensure(static_cast<size_t>(std::max<int64_t>(feed_floats, 1)) * sizeof(float));
     if (feed_floats)
