@@ -128,7 +128,7 @@ class FusedImpl : public FusedPlan {
         if (call.prof) {
             unsigned long long h[FS_COUNT + 4];
             cuda_check(cudaMemcpy(h, d_prof.p, sizeof h, cudaMemcpyDeviceToHost), "profile D2H");
-            static const char* names[FS_COUNT] = {"deferred", "in+conn", "sweep", "queue", "fixup",
+            static const char* names[FS_COUNT] = {"deferred", "in+conn", "sweep", "unit-barrier", "fixup",
                                                   "decode",   "barrier", "epilogue"};
             double tot = 0;
             for (int s = 0; s < FS_COUNT; ++s) tot += static_cast<double>(h[s]);

@@ -344,8 +344,9 @@ __device__ __noinline__ void dq_batch(const QEnt* q, int cnt, const FEns* e, flo
 /// acc = payload + T.src(kk) (sequential in j); f = a*state + b*acc; state = f.
 /// Returns f in f_out[r].  last: also write acc and filt to the arena.
 template <int DMAX, int BT>
-__device__ __forceinline__ void conn_rows(const FusedProgram& p, const FConn& cn, int kk, int b, int r_lo, int r_hi,
+__device__ __forceinline__ void conn_rows(const FusedProgram& p, const FConn& cn_g, int kk, int b, int r_lo, int r_hi,
                                           bool valid, bool last, float* f_out) {
+    const FConn cn = cn_g;  // a private copy: the fields stay in registers across the arena stores
     const int B = batch_of<BT>(p);
     float* A = p.arena;
     const float* src;
@@ -669,7 +670,7 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
                     dn += __popc(dm);
                 }
             }
-            if (dn >= 32) {  // warp-uniform
+            while (dn >= 32) {  // warp-uniform; keeps dn < 32 before the next pair (which adds <= 64)
                 dn -= 32;
                 __syncwarp();
                 tk.tick(FS_SWEEP);
@@ -809,6 +810,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_run_kernel(const __grid_con
             __syncthreads();
             const int u = *S.cur;
             __syncthreads();  // every thread has read cur before thread 0 claims again
+            tk.tick(FS_QUEUE);  // (profile: the unit barrier and claim)
             if (u >= units) break;  // uniform
             run_unit<DMAX, BT, PROF>(p, u, k, upd, last, S, parity, tk);
             parity ^= 1u;

@@ -181,3 +181,17 @@ def _two_shards_on_one_stream(pm, w, n, B, dev, stream):
             for b in (0, B - 1):
                 assert np.array_equal(owner.read_signal(sig[name], b).view(np.uint64),
                                       whole.read_signal(sig[name], b).view(np.uint64)), (name, b)
+
+
+def test_hard_driven_network_bit_exact_full_state():
+    # inputs x30: most neurons fire at their maximum rate and spike again on the step they leave
+    # the refractory period, so warp rows carry many lanes into the doubt queue at once (a pair
+    # of rows can push 64 entries: the queue must drain to < 32 before the next pair)
+    w = networks.random_network(9, n_ens=8, n=64, d=4, k_out=3, n_inputs=8, batch=64, steps=20)
+    feeds = {k: 30.0 * v for k, v in w.feeds.items()}
+    pm = passes.run_passes(w.model)
+    gpu = GpuEngine(pm, w.batch)
+    assert gpu.mode() == MODE_FUSED
+    ref = refapi.RefEngine(pm, w.batch)
+    assert_bitexact(gpu.run(w.steps, feeds), ref.run(w.steps, feeds), "hard driven")
+    full_state_equal(gpu, ref, pm.model, w.batch, "hard driven")
