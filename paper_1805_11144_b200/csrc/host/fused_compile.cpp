@@ -604,7 +604,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         // stage the decoder products with the encoders when shared memory
         // allows; prefer a footprint with two CTAs per SM
         {
-            constexpr size_t two = 113 * 1024, one = 227 * 1024;
+            constexpr size_t two = 75 * 1024, one = 227 * 1024;  // "two": the multi-CTA-per-SM budget (3 CTAs)
             p.stage_dec = 1;
             const size_t with = fused_smem_bytes(p, DMAX);
             p.stage_dec = 0;

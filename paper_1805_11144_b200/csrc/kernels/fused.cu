@@ -48,7 +48,8 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kUnroll = 8;   // neuron rows per prefetch round (pairs inside)
+constexpr int kUnroll = 4;   // neuron rows per prefetch round (pairs inside)
+constexpr int kMinBlocks = 3;  // CTAs per SM the register budget is sized for
 constexpr int kL2Ahead = 24; // rows of v/r pulled into L2 ahead of the round being computed
 constexpr uint32_t kFull = 0xffffffffu;
 
@@ -140,7 +141,7 @@ struct __align__(16) QEnt {
     uint32_t key;  // neuron << 5 | lane
     float a, b, c; // the step's original v, r, J
 };
-constexpr int kDQ = 96;  // per-warp doubt queue: <= 31 pending + 64 from a neuron pair
+constexpr int kDQ = 64;  // per-warp doubt queue: <= 31 pending + 32 from a neuron row
 
 struct Smem {
     uint64_t* bar;
@@ -574,7 +575,7 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
         for (int i = n0; i < n1; i += 2, vst += 2 * B, sE += 2 * DMAX, sbias += 2) {
             const int rel = i - n0;
             if ((rel & (kUnroll - 1)) == 0) {
-                const int st = (rel >> 3) & 1;
+                const int st = (rel / kUnroll) & 1;
                 __syncwarp();  // every lane's reads of the stage being refilled are done
                 ring_issue<BT>(RL, st ^ 1, i + kUnroll, n0, n1, B, vec);
                 cp_async_wait1();
@@ -669,14 +670,14 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
                     if (d) dq[dn + __popc(dm & lanemask_lt())] = QEnt{(static_cast<uint32_t>(i + h) << 5) | lane, vh, rh, J};
                     dn += __popc(dm);
                 }
-            }
-            while (dn >= 32) {  // warp-uniform; keeps dn < 32 before the next pair (which adds <= 64)
-                dn -= 32;
-                __syncwarp();
-                tk.tick(FS_SWEEP);
-                dq_batch(dq + dn, 32, p.ens + ei, A, B, b0, words, &p.libm, lane);
-                __syncwarp();
-                tk.tick(FS_FIX);
+                if (dn >= 32) {  // warp-uniform; a row adds <= 32, so dn < 32 before every row
+                    dn -= 32;
+                    __syncwarp();
+                    tk.tick(FS_SWEEP);
+                    dq_batch(dq + dn, 32, p.ens + ei, A, B, b0, words, &p.libm, lane);
+                    __syncwarp();
+                    tk.tick(FS_FIX);
+                }
             }
         }
         if (dn > 0) {
@@ -769,7 +770,7 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
 }
 
 template <int DMAX, int BT, bool PROF>
-__global__ void __launch_bounds__(kThreads, 2) fused_run_kernel(const __grid_constant__ FusedProgram p, int k_begin, int k_end) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) fused_run_kernel(const __grid_constant__ FusedProgram p, int k_begin, int k_end) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(128) uint32_t smem[];
     const Smem S = carve<DMAX>(smem, p);
