@@ -595,8 +595,9 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         p.libm = libm_tables(eng.device());
         // tiles per unit (one warp each) and warps per tile (neuron slices)
         {
-            int tu = 1;
-            while (tu < 8 && tu < p.btiles) tu *= 2;
+            int tu = 1, tu_max = 8;
+            if (const char* env = std::getenv("NENG_FUSED_TILES_PER_UNIT")) tu_max = std::max(1, std::min(8, std::atoi(env)));
+            while (tu < tu_max && tu < p.btiles) tu *= 2;
             p.tu = tu;
             p.slices = 8 / tu;
             p.groups = (p.btiles + tu - 1) / tu;

@@ -145,6 +145,7 @@ constexpr int kDQ = 64;  // per-warp doubt queue: <= 31 pending + 32 from a neur
 
 struct Smem {
     uint64_t* bar;
+    uint64_t* bar2;  // the decoder products' copy into the encoder region (when not staged up front)
     int* cur;      // the CTA's current unit
     float* E;      // nmax x DMAX (zero padded)
     float* bias;   // nmax
@@ -171,6 +172,7 @@ __device__ Smem carve(uint32_t* base, const FusedProgram& p) {
     char* at = reinterpret_cast<char*>(base);
     S.bar = reinterpret_cast<uint64_t*>(at);
     S.cur = reinterpret_cast<int*>(at + 8);
+    S.bar2 = reinterpret_cast<uint64_t*>(at + 16);
     at += 128;
     S.ring = reinterpret_cast<float*>(at);
     at += static_cast<size_t>(kWarps) * kRingFloats * 4;
@@ -704,10 +706,21 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
         }
     }
     tk.tick(FS_SWEEP);
-    if (p.slices > 1)
+    // the decoder products replace the encoders in shared memory once every warp
+    // is past its sweep (they are the same size or smaller: dx <= DMAX)
+    const bool p_late = !p.stage_dec;
+    if (p.slices > 1 || p_late)
         __syncthreads();
     else
         __syncwarp();
+    if (p_late) {
+        if (threadIdx.x == 0) {
+            fence_proxy_async_smem();  // the sweep's reads of the encoders are ordered first
+            mbar_expect_tx(S.bar2, static_cast<uint32_t>(e.dec_bytes));
+            bulk_g2s(S.E, p.values + e.dec_scaled_off, static_cast<uint32_t>(e.dec_bytes), S.bar2);
+        }
+        mbar_wait(S.bar2, parity);
+    }
 
     // 3. decode: rows [r0, r0 + R) of this warp's tile over all neurons, ascending
     if (active) {
@@ -717,7 +730,7 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
         const int r0 = slice * R;
         if (r0 < dx) {
             const int rn = min(R, dx - r0);
-            const float* Pb = (p.stage_dec ? S.P : p.values + e.dec_scaled_off) + r0;
+            const float* Pb = (p.stage_dec ? S.P : S.E) + r0;
             const bool vec = (dx & 3) == 0 && (rn & 3) == 0;
             float a[DMAX];
 #pragma unroll
@@ -774,7 +787,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fused_run_kernel(const _
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(128) uint32_t smem[];
     const Smem S = carve<DMAX>(smem, p);
-    if (threadIdx.x == 0) mbar_init(S.bar);
+    if (threadIdx.x == 0) {
+        mbar_init(S.bar);
+        mbar_init(S.bar2);
+    }
     for (uint32_t i = threadIdx.x; i < p.libm.t[0].n_regions; i += blockDim.x) S.w8e[i] = p.libm.t[0].region_w8[i];
     for (uint32_t i = threadIdx.x; i < p.libm.t[1].n_regions; i += blockDim.x) S.w8l[i] = p.libm.t[1].region_w8[i];
     __syncthreads();
