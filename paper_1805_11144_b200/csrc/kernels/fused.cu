@@ -138,9 +138,10 @@ struct Ticker {
 };
 
 struct __align__(16) QEnt {
-    uint32_t key;  // neuron << 5 | lane
+    uint32_t key;  // neuron << 5 | lane, | kDoubtExp / kDoubtLog: which speculative value was doubtful
     float a, b, c; // the step's original v, r, J
 };
+constexpr uint32_t kDoubtExp = 0x80000000u, kDoubtLog = 0x40000000u;
 constexpr int kDQ = 64;  // per-warp doubt queue: <= 31 pending + 32 from a neuron row
 
 struct Smem {
@@ -322,23 +323,72 @@ __device__ __forceinline__ bool lif_exact(float J, float& v, float& r, float dt,
     return false;
 }
 
-/// Doubtful values (out of line: ~5% of the transcendentals): lif_spike_step
-/// recomputed exactly from the original v, r, J; patches v, r and the spike
-/// bit.  Lane l takes entry l of q[0, cnt).  Called from the sweep every 32
-/// entries, so its latency overlaps the other warps' sweeps.
-__device__ __noinline__ void dq_batch(const QEnt* q, int cnt, const FEns* e, float* A, int B, int b0,
-                                      uint32_t* words, const LibmTables* lt, int lane) {
-    if (lane >= cnt) return;
-    const QEnt x = q[lane];
-    const uint32_t i = x.key >> 5, col = x.key & 31u;
+/// Doubtful values (out of line: ~5% of the transcendentals).  The sweep
+/// stored the speculative v, r and spike bit.  A speculative value is glibc's
+/// unless its argument is table-listed, so the entry first re-derives the
+/// doubtful argument (cheap: the expm1 argument from r, the log1p argument
+/// from the refractory-free voltage) and asks the block filter; only a
+/// listed, out-of-range or compound case (a doubtful log1p after an exit)
+/// recomputes the step exactly and patches v, r and the spike bit.
+/// Lane l takes entry l of q[0, cnt).
+/// The exact step of one doubtful lane (out of line and rare: its code stays
+/// out of the sweep's instruction-cache footprint).
+__device__ __noinline__ void dq_exact(uint32_t key, float v, float r, float J, const FEns* e, float* A, int B, int b0,
+                                      uint32_t* words, const LibmTables* lt) {
+    const uint32_t i = key >> 5, col = key & 31u;
     const int64_t o = static_cast<int64_t>(i) * B + b0 + col;
-    float v = x.a, r = x.b;
-    if (lif_exact(x.c, v, r, e->dt, e->tau_rc, e->tau_ref, *lt))
+    if (lif_exact(J, v, r, e->dt, e->tau_rc, e->tau_ref, *lt))
         atomicOr(words + i, 1u << col);
     else
         atomicAnd(words + i, ~(1u << col));
     A[e->v_base + o] = v;
     A[e->r_base + o] = r;
+}
+
+/// Step constants of an ensemble the doubt resolution needs (passed in
+/// registers: re-reading them from the FEns in global memory put an L2 round
+/// trip in front of every batch).
+struct DqConst {
+    float dt, em_dt;
+    double inv_tau_rc;
+    const uint32_t* filt_e;  // block filters of the expm1 / log1p LIF-range tables
+    const uint32_t* filt_l;
+};
+
+/// One batch of doubtful lanes (lane l takes entry l of q[0, cnt)).  The
+/// sweep stored the speculative v, r and spike bit.  A speculative value is
+/// glibc's unless its argument is table-listed, so the entry re-derives the
+/// doubtful argument (cheap: the expm1 argument from r, the log1p argument from
+/// the refractory-free voltage) and asks the block filter; only a maybe-listed,
+/// out-of-range or compound case (a doubtful log1p after an exit) takes the
+/// exact path.
+__device__ __forceinline__ void dq_batch(const QEnt* q, int cnt, const DqConst& K, const FEns* e, float* A, int B,
+                                         int b0, uint32_t* words, const LibmTables* lt, int lane) {
+    if (lane >= cnt) return;
+    const QEnt x = q[lane];
+    const bool de = x.key & kDoubtExp, dl = x.key & kDoubtLog;
+    const uint32_t key = x.key & ~(kDoubtExp | kDoubtLog);
+    const float dt = K.dt, v0 = x.a, r0 = x.b, J = x.c;
+    const float delta = dt - r0;
+    const bool ge = delta >= dt, le = delta <= 0.0f, ex = !ge && !le;
+    bool exact = dl && ex;  // the log1p argument depends on a speculative expm1: recompute all
+    if (!exact) {
+        float arg;
+        const uint32_t* filt;
+        if (de) {
+            arg = static_cast<float>(static_cast<double>(-delta) * K.inv_tau_rc);  // == -delta / tau_rc (sweep)
+            filt = K.filt_e;
+        } else {
+            float vn = v0 - (J - v0) * (ge ? K.em_dt : -0.0f);
+            if (vn < 0.0f) vn = 0.0f;
+            arg = -(vn - 1.0f) / (J - 1.0f);
+            filt = K.filt_l;
+        }
+        const uint32_t k = __float_as_uint(arg) - 0x80000001u;  // LIF range <=> k <= 0x3D7FFFFF
+        exact = k > 0x3D7FFFFFu || ((__ldg(filt + (k >> 11)) >> ((k >> 6) & 31u)) & 1u);
+        // a set filter bit only says "maybe listed": dq_exact decides (exactly) either way
+    }
+    if (exact) dq_exact(key, v0, r0, J, e, A, B, b0, words, lt);  // the speculative values stand otherwise
 }
 
 // ---- connections ----------------------------------------------------------
@@ -570,6 +620,7 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
         }
         ring_issue<BT>(RL, 0, n0, n0, n1, B, vec);
         const bool lv = (BT > 0 && BT % 32 == 0) ? true : valid;  // inside the sweep the tile is active
+        const DqConst dqk{dt, em_dt, inv_tau_rc, lt.t[0].hot_filter, lt.t[1].hot_filter};
         const uint32_t sh_e = lt.t[0].region_shift, sh_l = lt.t[1].region_shift;
         const float* ring_l = ring + lane;
         const float* sE = S.E + n0 * DMAX;
@@ -661,7 +712,7 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
                 const bool d = row && (dbt[h] || (spike && sl.doubtful));
                 const float since = -tau_rc * sl.r;
                 const float rn = spike ? tau_ref - since : (rh > dt ? (h ? rr2.y : rr2.x) : 0.0f);
-                if (row && !d) {  // doubtful lanes are written by the resolution
+                if (row) {  // doubtful lanes too: their speculative values usually stand (see dq_batch)
                     __stcs(vst + h * B, spike ? 0.0f : vn);
                     __stcs(vst + h * B + rdelta, rn);
                 }
@@ -669,14 +720,18 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
                 if (lane == 0 && (h == 0 || two)) words[i + h] = word;
                 const uint32_t dm = __ballot_sync(kFull, d);
                 if (dm) {  // warp-uniform
-                    if (d) dq[dn + __popc(dm & lanemask_lt())] = QEnt{(static_cast<uint32_t>(i + h) << 5) | lane, vh, rh, J};
+                    if (d)
+                        dq[dn + __popc(dm & lanemask_lt())] =
+                            QEnt{(static_cast<uint32_t>(i + h) << 5) | lane | (dbt[h] ? kDoubtExp : 0u) |
+                                     (spike && sl.doubtful ? kDoubtLog : 0u),
+                                 vh, rh, J};
                     dn += __popc(dm);
                 }
                 if (dn >= 32) {  // warp-uniform; a row adds <= 32, so dn < 32 before every row
                     dn -= 32;
                     __syncwarp();
                     tk.tick(FS_SWEEP);
-                    dq_batch(dq + dn, 32, p.ens + ei, A, B, b0, words, &p.libm, lane);
+                    dq_batch(dq + dn, 32, dqk, p.ens + ei, A, B, b0, words, &p.libm, lane);
                     __syncwarp();
                     tk.tick(FS_FIX);
                 }
@@ -684,7 +739,7 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
         }
         if (dn > 0) {
             __syncwarp();
-            dq_batch(dq, dn, p.ens + ei, A, B, b0, words, &p.libm, lane);
+            dq_batch(dq, dn, dqk, p.ens + ei, A, B, b0, words, &p.libm, lane);
             __syncwarp();
             dn = 0;
         }
