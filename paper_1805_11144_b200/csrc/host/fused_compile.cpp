@@ -136,6 +136,8 @@ class FusedImpl : public FusedPlan {
             for (int s = 0; s < FS_COUNT; ++s)
                 std::fprintf(stderr, " %s=%.1f", names[s], h[s] / 1e3 / grid / n_steps);
             std::fprintf(stderr, " (total %.1f)\n", tot / 1e3 / grid / n_steps);
+            std::fprintf(stderr, "[fused profile] per step: doubt entries %.0f, exact path %.0f\n",
+                         double(h[FS_COUNT]) / n_steps, double(h[FS_COUNT + 1]) / n_steps);
         }
         return launches;
     }

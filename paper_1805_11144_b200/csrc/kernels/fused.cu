@@ -93,7 +93,10 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 /// Pull `bytes` (multiple of 16, 16-B aligned) of global memory into L2 (TMA prefetch).
 __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol)
+                 : "memory");
 }
 __device__ __forceinline__ void prefetch_l2_line(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
@@ -231,8 +234,27 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
+// L2 policies: the streamed neuron state is evict-first, so the libm tables the
+// doubt resolution probes (a few MB) stay L2-resident next to 2 GB/step of v, r
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t l2_evict_last() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                 "l"(l2_evict_first())
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t ldg_keep(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(l2_evict_last()));
+    return v;
 }
 __device__ __forceinline__ void cp_async4_s(uint32_t dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
@@ -353,6 +375,7 @@ struct DqConst {
     double inv_tau_rc;
     const uint32_t* filt_e;  // block filters of the expm1 / log1p LIF-range tables
     const uint32_t* filt_l;
+    unsigned long long* prof;  // profile builds: counters (else null)
 };
 
 /// One batch of doubtful lanes (lane l takes entry l of q[0, cnt)).  The
@@ -385,8 +408,12 @@ __device__ __forceinline__ void dq_batch(const QEnt* q, int cnt, const DqConst& 
             filt = K.filt_l;
         }
         const uint32_t k = __float_as_uint(arg) - 0x80000001u;  // LIF range <=> k <= 0x3D7FFFFF
-        exact = k > 0x3D7FFFFFu || ((__ldg(filt + (k >> 11)) >> ((k >> 6) & 31u)) & 1u);
+        exact = k > 0x3D7FFFFFu || ((ldg_keep(filt + (k >> 11)) >> ((k >> 6) & 31u)) & 1u);
         // a set filter bit only says "maybe listed": dq_exact decides (exactly) either way
+    }
+    if (K.prof) {  // profile builds: doubt entries, exact-path entries
+        atomicAdd(K.prof, 1ull);
+        if (exact) atomicAdd(K.prof + 1, 1ull);
     }
     if (exact) dq_exact(key, v0, r0, J, e, A, B, b0, words, lt);  // the speculative values stand otherwise
 }
@@ -620,7 +647,8 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
         }
         ring_issue<BT>(RL, 0, n0, n0, n1, B, vec);
         const bool lv = (BT > 0 && BT % 32 == 0) ? true : valid;  // inside the sweep the tile is active
-        const DqConst dqk{dt, em_dt, inv_tau_rc, lt.t[0].hot_filter, lt.t[1].hot_filter};
+        const DqConst dqk{dt, em_dt, inv_tau_rc, lt.t[0].hot_filter, lt.t[1].hot_filter,
+                          PROF ? p.prof + FS_COUNT : nullptr};
         const uint32_t sh_e = lt.t[0].region_shift, sh_l = lt.t[1].region_shift;
         const float* ring_l = ring + lane;
         const float* sE = S.E + n0 * DMAX;
