@@ -29,6 +29,8 @@ cudaError_t launch_reset(float* arena, const float* pristine, const int64_t* bas
                          const int64_t* span, const int32_t* per_batch, int nbuf, int B, cudaStream_t stream);
 cudaError_t launch_probe_transpose(const float* ring, float* out, const int64_t* off, const int32_t* dims,
                                    int nprobes, int steps, int B, cudaStream_t stream);
+cudaError_t launch_feed_transpose(const float* in, float* out, const int64_t* offs, const int32_t* cols, int nslots,
+                                  int max_cols, int B, cudaStream_t stream);
 cudaError_t launch_libm_hash_build(unsigned long long* slots, uint32_t mask, int shift, const uint32_t* keys,
                                    const uint32_t* results, int64_t n, cudaStream_t stream);
 
@@ -300,6 +302,8 @@ Engine::Engine(PlannedModel planned, int batch, int unroll, const neng_device_cf
 Engine::~Engine() {
     fused_.reset();
     if (cublas_) cublasDestroy(static_cast<cublasHandle_t>(cublas_));
+    for (cudaEvent_t& ev : feed_events_)
+        if (ev) cudaEventDestroy(ev);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -718,48 +722,97 @@ void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probe
             feed_floats += static_cast<int64_t>(n_steps) * feeds_[f].dim * B;
         }
     }
-    feed_stage_.ensure(static_cast<size_t>(std::max<int64_t>(feed_floats, 1)) * sizeof(float));
-    float* stage = feed_stage_.as<float>();
-    {
-        // transpose + narrow on the host cores: slot blocks are independent
-        std::vector<std::pair<size_t, int64_t>> jobs;  // (slot, offset in the stage)
-        int64_t at = 0;
-        for (size_t f = 0; f < feeds_.size(); ++f) {
-            if (!present[f]) continue;
-            jobs.emplace_back(f, at);
-            at += static_cast<int64_t>(n_steps) * feeds_[f].dim * B;
-        }
-        auto work = [&](size_t j0, size_t j1) {
-            for (size_t j = j0; j < j1; ++j) {
-                const auto [f, off] = jobs[j];
-                const neng_feed* t = src[f];
-                const int dim = feeds_[f].dim;
-                for (int s = 0; s < n_steps; ++s)
-                    for (int d = 0; d < dim; ++d) {
-                        float* row = stage + off + (static_cast<int64_t>(s) * dim + d) * B;
-                        for (int b = 0; b < B; ++b)
-                            row[b] = static_cast<float>(t->data[(static_cast<int64_t>(b) * t->steps + s) * t->dim + d]);
-                    }
-            }
-        };
-        const size_t nt = std::min<size_t>(jobs.size(), std::max(1u, std::thread::hardware_concurrency()));
-        if (nt <= 1 || feed_floats < (int64_t{1} << 20)) {
-            work(0, jobs.size());
-        } else {
-            std::vector<std::thread> pool;
-            for (size_t t = 0; t < nt; ++t) pool.emplace_back(work, jobs.size() * t / nt, jobs.size() * (t + 1) / nt);
-            for (auto& th : pool) th.join();
-        }
-    }
-    feed_buf_.ensure(static_cast<size_t>(std::max<int64_t>(feed_floats, 1)) * sizeof(float));
-    if (feed_floats)
-        cuda_check(cudaMemcpyAsync(feed_buf_.p, stage, feed_floats * sizeof(float), cudaMemcpyHostToDevice, stream_),
-                   "feed H2D");
     int64_t ring_floats = 0;
     for (const DProbe& q : probes_) ring_floats += static_cast<int64_t>(n_steps) * q.dim * B;
     ring_.ensure(static_cast<size_t>(std::max<int64_t>(ring_floats, 1)) * sizeof(float));
 
-    launch_steps(n_steps, feed_buf_.as<float>(), present, ring_.as<float>(), stream_);
+    // Feeds: narrowed f64 -> f32 on the host cores in the host's own order ([b][step][dim],
+    // contiguous per batch row), copied, and transposed to [step][dim][B] on the device, in
+    // chunks of steps; with the fused pipeline chunk c+1 is staged while chunk c runs.
+    std::vector<int64_t> full_off, ring_off;
+    call_offsets(n_steps, present, &full_off, &ring_off);
+    int64_t per_step = 0;  // floats per step over the present slots
+    std::vector<size_t> slots;
+    for (size_t f = 0; f < feeds_.size(); ++f)
+        if (present[f]) {
+            slots.push_back(f);
+            per_step += static_cast<int64_t>(feeds_[f].dim) * B;
+        }
+    int cs = n_steps;
+    if (fused_ && per_step > 0) cs = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(n_steps, (int64_t{1} << 23) / per_step)));
+    const int nbuf = cs < n_steps ? 2 : 1;
+    feed_buf_.ensure(static_cast<size_t>(std::max<int64_t>(feed_floats, 1)) * sizeof(float));
+    const size_t chunk_floats = static_cast<size_t>(std::max<int64_t>(per_step * cs, 1));
+    feed_stage_.ensure(chunk_floats * nbuf * sizeof(float));
+    feed_raw_.ensure(chunk_floats * nbuf * sizeof(float));
+    feed_meta_.ensure((slots.size() * 20 + 16) * nbuf);
+    if (!feed_events_[0]) {
+        cuda_check(cudaEventCreateWithFlags(&feed_events_[0], cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&feed_events_[1], cudaEventDisableTiming), "cudaEventCreate");
+    }
+    auto stage_chunk = [&](int c0, int c1, int buf) {
+        if (slots.empty()) return;
+        const int n = c1 - c0;
+        float* stage = feed_stage_.as<float>() + chunk_floats * buf;
+        float* raw = feed_raw_.as<float>() + chunk_floats * buf;
+        cuda_check(cudaEventSynchronize(feed_events_[buf]), "feed staging buffer");  // its last copy is done
+        std::vector<int64_t> offs(2 * slots.size());
+        std::vector<int32_t> cols(slots.size());
+        int64_t at = 0;
+        for (size_t j = 0; j < slots.size(); ++j) {
+            const size_t f = slots[j];
+            offs[j] = at;
+            offs[slots.size() + j] = full_off[f] + static_cast<int64_t>(c0) * feeds_[f].dim * B;
+            cols[j] = n * feeds_[f].dim;
+            at += static_cast<int64_t>(n) * feeds_[f].dim * B;
+        }
+        const int64_t rows = static_cast<int64_t>(slots.size()) * B;  // (slot, batch row) pieces
+        auto work = [&](int64_t q0, int64_t q1) {
+            for (int64_t q = q0; q < q1; ++q) {
+                const size_t j = static_cast<size_t>(q / B);
+                const int b = static_cast<int>(q % B);
+                const neng_feed* t = src[slots[j]];
+                const int64_t len = static_cast<int64_t>(n) * t->dim;
+                const double* in = t->data + (static_cast<int64_t>(b) * t->steps + c0) * t->dim;
+                float* out = stage + offs[j] + static_cast<int64_t>(b) * len;
+                for (int64_t i = 0; i < len; ++i) out[i] = static_cast<float>(in[i]);
+            }
+        };
+        const int64_t nt = std::min<int64_t>(rows, std::max(1u, std::thread::hardware_concurrency()));
+        if (nt <= 1 || at < (int64_t{1} << 20)) {
+            work(0, rows);
+        } else {
+            std::vector<std::thread> pool;
+            for (int64_t t = 0; t < nt; ++t) pool.emplace_back(work, rows * t / nt, rows * (t + 1) / nt);
+            for (auto& th : pool) th.join();
+        }
+        char* meta = feed_meta_.as<char>() + (slots.size() * 20 + 16) * buf;
+        cuda_check(cudaMemcpyAsync(raw, stage, at * sizeof(float), cudaMemcpyHostToDevice, stream_), "feed H2D");
+        cuda_check(cudaMemcpyAsync(meta, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice, stream_), "feed meta");
+        cuda_check(cudaMemcpyAsync(meta + offs.size() * 8, cols.data(), cols.size() * 4, cudaMemcpyHostToDevice,
+                                   stream_),
+                   "feed meta");
+        cuda_check(cudaEventRecord(feed_events_[buf], stream_), "feed event");
+        const int max_cols = *std::max_element(cols.begin(), cols.end());
+        cuda_check(launch_feed_transpose(raw, feed_buf_.as<float>(), reinterpret_cast<const int64_t*>(meta),
+                                         reinterpret_cast<const int32_t*>(meta + offs.size() * 8),
+                                         static_cast<int>(slots.size()), max_cols, B, stream_),
+                   "feed transpose");
+    };
+    if (fused_ && cs < n_steps) {
+        fused_->begin(n_steps, feed_buf_.as<float>(), full_off.data(), present.data(), ring_.as<float>(),
+                      ring_off.data(), stream_);
+        last_launches_ = 0;
+        for (int c0 = 0, i = 0; c0 < n_steps; c0 += cs, ++i) {
+            const int c1 = std::min(n_steps, c0 + cs);
+            stage_chunk(c0, c1, i & 1);
+            fused_->launch(c0, c1, NENG_STEP_EPILOGUE, stream_);
+            ++last_launches_;
+        }
+    } else {
+        stage_chunk(0, n_steps, 0);
+        launch_steps(n_steps, feed_buf_.as<float>(), present, ring_.as<float>(), stream_);
+    }
 
     if (ring_floats) {
         // ring [probe][step][dim][B] -> [probe][B][step][dim], D2H, widen to f64

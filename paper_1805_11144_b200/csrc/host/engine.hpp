@@ -150,7 +150,8 @@ class Engine {
     std::unique_ptr<FusedPlan> fused_;
 
     // per-call scratch
-    DevMem feed_buf_, ring_, probe_out_, probe_meta_;
+    DevMem feed_buf_, feed_raw_, feed_meta_, ring_, probe_out_, probe_meta_;
+    cudaEvent_t feed_events_[2] = {nullptr, nullptr};  // staging-buffer reuse (pipelined host feeds)
     PinnedMem feed_stage_, probe_stage_;
 };
 

@@ -31,6 +31,8 @@ struct FusedPlan {
     virtual void begin(int n_steps, const float* d_feed_data, const int64_t* feed_off, const int* present,
                        float* d_ring, const int64_t* ring_off, cudaStream_t stream) = 0;
     virtual void step(int k, int flags, cudaStream_t stream) = 0;
+    // steps [k0, k1) of the open call in one launch (same flags as step)
+    virtual void launch(int k0, int k1, int flags, cudaStream_t stream) = 0;
     virtual void xhat_layout(int64_t* xbuf_floats, int64_t* rank_floats, float** xbuf) const = 0;
     virtual void set_xhat_buffer(float* d_buf) = 0;
 };

@@ -90,12 +90,15 @@ class FusedImpl : public FusedPlan {
     }
 
     void step(int k, int flags, cudaStream_t stream) override {
+        launch(k, k < call.call_steps ? k + 1 : k, flags, stream);  // k == n_steps: the epilogue of step n - 1
+    }
+
+    void launch(int k0, int k1, int flags, cudaStream_t stream) override {
         FusedProgram p = call;
         p.first_update = (flags & NENG_STEP_FIRST_UPDATE) ? 1 : 0;
         p.epilogue = (flags & NENG_STEP_EPILOGUE) ? 1 : 0;
-        const int k1 = k < p.call_steps ? k + 1 : k;  // k == n_steps: the epilogue of step n - 1 only
         cuda_check(cudaMemsetAsync(d_work.p, 0, 8, stream), "fused work reset");
-        cuda_check(launch_fused(p, dmax, grid, k, k1, stream), "fused kernel launch");
+        cuda_check(launch_fused(p, dmax, grid, k0, k1, stream), "fused kernel launch");
     }
 
     void xhat_layout(int64_t* xbuf_floats, int64_t* rank_floats, float** xbuf) const override {

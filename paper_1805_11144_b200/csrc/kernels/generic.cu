@@ -332,6 +332,41 @@ int generic_max_coresident_blocks(int device) {
     return per_sm * sms;
 }
 
+// feed staging: per present slot, [B][steps*dim] (the host's Tensor3 order,
+// narrowed to f32) -> [steps*dim][B] (the device order), 32x32 tiles through
+// smem; offs holds nslots input offsets then nslots output offsets
+__global__ void feed_transpose_kernel(const float* in, float* out, const int64_t* offs, const int32_t* cols, int nslots,
+                                      int B) {
+    __shared__ float tile[32][33];
+    for (int s = blockIdx.z; s < nslots; s += gridDim.z) {
+        const int C = cols[s];  // steps * dim of this block
+        const float* src = in + offs[s];           // [B][C]
+        float* dst = out + offs[nslots + s];       // [C][B]
+        for (int cb = blockIdx.x * 32; cb < C; cb += gridDim.x * 32)
+            for (int bb = blockIdx.y * 32; bb < B; bb += gridDim.y * 32) {
+                for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+                    const int b = bb + r, c = cb + threadIdx.x;
+                    tile[r][threadIdx.x] = (b < B && c < C) ? src[static_cast<int64_t>(b) * C + c] : 0.0f;
+                }
+                __syncthreads();
+                for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+                    const int c = cb + r, b = bb + threadIdx.x;
+                    if (b < B && c < C) dst[static_cast<int64_t>(c) * B + b] = tile[threadIdx.x][r];
+                }
+                __syncthreads();
+            }
+    }
+}
+
+cudaError_t launch_feed_transpose(const float* in, float* out, const int64_t* offs, const int32_t* cols, int nslots,
+                                  int max_cols, int B, cudaStream_t stream) {
+    if (nslots == 0) return cudaSuccess;
+    dim3 grid((max_cols + 31) / 32 < 64 ? (max_cols + 31) / 32 : 64, (B + 31) / 32 < 16 ? (B + 31) / 32 : 16,
+              nslots < 1024 ? nslots : 1024);
+    feed_transpose_kernel<<<grid, dim3(32, 8), 0, stream>>>(in, out, offs, cols, nslots, B);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_reset(float* arena, const float* pristine, const int64_t* base, const int64_t* pbase,
                          const int64_t* span, const int32_t* per_batch, int nbuf, int B, cudaStream_t stream) {
     if (nbuf == 0) return cudaSuccess;
