@@ -210,6 +210,42 @@ const LibmTables& libm_tables(int device) {
         build(ht.keys.data() + a, ht.results.data() + a, b > a ? b - a : 0, &dl->tables.t[t].hot_slots,
               &dl->tables.t[t].hot_mask, &dl->tables.t[t].hot_shift);
         {
+            // bucketed key set of the same LIF-range keys (load <= 1/4 per slot on average)
+            const size_t nk = b > a ? b - a : 0;
+            int lb = 4;
+            while ((size_t{4} << lb) < 4 * nk + 64) ++lb;  // 4 * 2^lb slots >= 4 * nk: load <= 0.25
+            const size_t nb = size_t{1} << lb;
+            std::vector<uint32_t> bk(nb * 4, 0u), br(nb * 4, 0u);
+            for (size_t q = a; q < b; ++q) {
+                const uint32_t key = ht.keys[q];
+                const uint32_t res = ht.results[q];
+                size_t bi = static_cast<uint32_t>(key * 0x9E3779B1u) >> (32 - lb);
+                for (;;) {
+                    uint32_t* slot = bk.data() + bi * 4;
+                    int j = 0;
+                    while (j < 4 && slot[j] != 0u) ++j;
+                    if (j < 4) {
+                        slot[j] = key;
+                        br[bi * 4 + j] = res;
+                        break;
+                    }
+                    bi = (bi + 1) & (nb - 1);
+                }
+            }
+            void* db = nullptr;
+            cuda_check(cudaMalloc(&db, bk.size() * 4), "cudaMalloc libm buckets");
+            cuda_check(cudaMemcpy(db, bk.data(), bk.size() * 4, cudaMemcpyHostToDevice), "libm buckets H2D");
+            dl->allocs.push_back(db);
+            dl->tables.t[t].hot_buckets = static_cast<const uint4*>(db);
+            void* dr2 = nullptr;
+            cuda_check(cudaMalloc(&dr2, br.size() * 4), "cudaMalloc libm bucket results");
+            cuda_check(cudaMemcpy(dr2, br.data(), br.size() * 4, cudaMemcpyHostToDevice), "libm bucket results H2D");
+            dl->allocs.push_back(dr2);
+            dl->tables.t[t].bucket_results = static_cast<const uint32_t*>(dr2);
+            dl->tables.t[t].bucket_mask = static_cast<uint32_t>(nb - 1);
+            dl->tables.t[t].bucket_shift = 32 - lb;
+        }
+        {
             // block filter over k = key - 0x80000001 in [0, 0x3D800000): bit (k >> 6)
             std::vector<uint32_t> filt((0x3D800000u >> 11) + 1, 0u);
             for (size_t q = a; q < b; ++q) {

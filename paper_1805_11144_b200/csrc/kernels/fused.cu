@@ -373,49 +373,91 @@ __device__ __noinline__ void dq_exact(uint32_t key, float v, float r, float J, c
 struct DqConst {
     float dt, em_dt;
     double inv_tau_rc;
-    const uint32_t* filt_e;  // block filters of the expm1 / log1p LIF-range tables
-    const uint32_t* filt_l;
+    const uint4* bk_e;  // bucketed LIF-range key sets of expm1 / log1p
+    const uint4* bk_l;
+    const uint32_t* br_e;  // their glibc results
+    const uint32_t* br_l;
+    float tau_rc, tau_ref;
+    float* vcol;     // v of row 0 of this tile's column 0 (A + v_base + b0)
+    int64_t rdelta;  // r_base - v_base
+    const uint8_t* w8e;  // the shared-memory screening tables (spec_any)
+    const uint8_t* w8l;
+    uint32_t w8_shift;
+    uint32_t bmask_e, bmask_l;
+    int bshift_e, bshift_l;
     unsigned long long* prof;  // profile builds: counters (else null)
 };
 
-/// One batch of doubtful lanes (lane l takes entry l of q[0, cnt)).  The
-/// sweep stored the speculative v, r and spike bit.  A speculative value is
-/// glibc's unless its argument is table-listed, so the entry re-derives the
-/// doubtful argument (cheap: the expm1 argument from r, the log1p argument from
-/// the refractory-free voltage) and asks the block filter; only a maybe-listed,
-/// out-of-range or compound case (a doubtful log1p after an exit) takes the
-/// exact path.
+/// glibc's value of expm1f / log1pf (is_log) at x on the LIF range, without the
+/// slow paths: the rounded polynomial unless it is doubtful and x is listed in
+/// the bucketed table (then the table value).  Returns false when only the
+/// exact path can decide (x outside the LIF range, or a full bucket).
+__device__ __forceinline__ bool glibc_fast(float x, bool is_log, const DqConst& K, float* out) {
+    const Spec sp = spec_any(x, is_log, is_log ? K.w8l : K.w8e, K.w8_shift);
+    *out = sp.r;
+    if (!sp.doubtful) return true;
+    const uint32_t ka = __float_as_uint(x);
+    if (ka - 0x80000001u > 0x3D7FFFFFu) return false;  // outside the LIF range
+    const uint32_t bi = (ka * 0x9E3779B1u) >> (is_log ? K.bshift_l : K.bshift_e);
+    const uint4 bk = __ldg((is_log ? K.bk_l : K.bk_e) + bi);
+    const int j = bk.x == ka ? 0 : bk.y == ka ? 1 : bk.z == ka ? 2 : bk.w == ka ? 3 : -1;
+    if (j < 0) return !(bk.x && bk.y && bk.z && bk.w);  // not listed (its home bucket has room)
+    *out = __uint_as_float(__ldg((is_log ? K.br_l : K.br_e) + bi * 4 + j));  // listed: glibc's value
+    return true;
+}
+
+/// One batch of doubtful lanes (lane l takes entry l of q[0, cnt)): the step
+/// recomputed from the original v, r, J with glibc_fast for the transcendentals
+/// (the bucketed table instead of the exact path's probes); v, r and the spike
+/// bit are rewritten.  Only arguments outside the LIF range or full buckets
+/// fall through to dq_exact.
 __device__ __forceinline__ void dq_batch(const QEnt* q, int cnt, const DqConst& K, const FEns* e, float* A, int B,
                                          int b0, uint32_t* words, const LibmTables* lt, int lane) {
     if (lane >= cnt) return;
     const QEnt x = q[lane];
-    const bool de = x.key & kDoubtExp, dl = x.key & kDoubtLog;
     const uint32_t key = x.key & ~(kDoubtExp | kDoubtLog);
     const float dt = K.dt, v0 = x.a, r0 = x.b, J = x.c;
-    const float delta = dt - r0;
-    const bool ge = delta >= dt, le = delta <= 0.0f, ex = !ge && !le;
-    bool exact = dl && ex;  // the log1p argument depends on a speculative expm1: recompute all
-    if (!exact) {
-        float arg;
-        const uint32_t* filt;
-        if (de) {
-            arg = static_cast<float>(static_cast<double>(-delta) * K.inv_tau_rc);  // == -delta / tau_rc (sweep)
-            filt = K.filt_e;
-        } else {
-            float vn = v0 - (J - v0) * (ge ? K.em_dt : -0.0f);
-            if (vn < 0.0f) vn = 0.0f;
-            arg = -(vn - 1.0f) / (J - 1.0f);
-            filt = K.filt_l;
-        }
-        const uint32_t k = __float_as_uint(arg) - 0x80000001u;  // LIF range <=> k <= 0x3D7FFFFF
-        exact = k > 0x3D7FFFFFu || ((ldg_keep(filt + (k >> 11)) >> ((k >> 6) & 31u)) & 1u);
-        // a set filter bit only says "maybe listed": dq_exact decides (exactly) either way
+    // lif_spike_step<float> (neuron_math.hpp:55-77)
+    float delta = dt - r0;
+    if (delta < 0.0f) delta = 0.0f;
+    if (delta > dt) delta = dt;
+    bool ok = true;
+    float em;
+    if (delta == dt) {
+        em = K.em_dt;
+    } else if (delta == 0.0f) {
+        em = -0.0f;
+    } else {
+        const float xa = static_cast<float>(static_cast<double>(-delta) * K.inv_tau_rc);  // == -delta / tau_rc
+        ok = glibc_fast(xa, false, K, &em);
+    }
+    float vn = v0 - (J - v0) * em;
+    if (vn < 0.0f) vn = 0.0f;
+    const bool spike = vn > 1.0f;
+    float v = vn, r = r0 > dt ? r0 - dt : 0.0f;
+    if (ok && spike) {
+        float lg;
+        ok = glibc_fast(-(vn - 1.0f) / (J - 1.0f), true, K, &lg);
+        const float since = -K.tau_rc * lg;
+        v = 0.0f;
+        r = K.tau_ref - since;
     }
     if (K.prof) {  // profile builds: doubt entries, exact-path entries
         atomicAdd(K.prof, 1ull);
-        if (exact) atomicAdd(K.prof + 1, 1ull);
+        if (!ok) atomicAdd(K.prof + 1, 1ull);
     }
-    if (exact) dq_exact(key, v0, r0, J, e, A, B, b0, words, lt);  // the speculative values stand otherwise
+    if (!ok) {
+        dq_exact(key, v0, r0, J, e, A, B, b0, words, lt);
+        return;
+    }
+    const uint32_t i = key >> 5, col = key & 31u;
+    float* vp = K.vcol + static_cast<int64_t>(i) * B + col;
+    vp[0] = v;
+    vp[K.rdelta] = r;
+    if (spike)
+        atomicOr(words + i, 1u << col);
+    else
+        atomicAnd(words + i, ~(1u << col));
 }
 
 // ---- connections ----------------------------------------------------------
@@ -647,7 +689,10 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
         }
         ring_issue<BT>(RL, 0, n0, n0, n1, B, vec);
         const bool lv = (BT > 0 && BT % 32 == 0) ? true : valid;  // inside the sweep the tile is active
-        const DqConst dqk{dt, em_dt, inv_tau_rc, lt.t[0].hot_filter, lt.t[1].hot_filter,
+        const DqConst dqk{dt, em_dt, inv_tau_rc, lt.t[0].hot_buckets, lt.t[1].hot_buckets, lt.t[0].bucket_results,
+                          lt.t[1].bucket_results, tau_rc, tau_ref, vrow0, rdelta, S.w8e, S.w8l, lt.t[0].region_shift,
+                          lt.t[0].bucket_mask,
+                          lt.t[1].bucket_mask, lt.t[0].bucket_shift, lt.t[1].bucket_shift,
                           PROF ? p.prof + FS_COUNT : nullptr};
         const uint32_t sh_e = lt.t[0].region_shift, sh_l = lt.t[1].region_shift;
         const float* ring_l = ring + lane;

@@ -12,6 +12,8 @@
 
 #include <cstdint>
 
+#include <vector_types.h>  // uint4
+
 namespace nengb {
 
 struct DArg {
@@ -87,6 +89,13 @@ struct LibmHash {
     // hot-table key (2 MB, L2-resident); a clear bit answers "not listed"
     // without probing the hash table
     const uint32_t* hot_filter = nullptr;
+    // the same LIF-range key set as 4-key buckets (one 16-B load answers "listed?"
+    // unless the bucket is full): bucket = (key * 0x9E3779B1) >> bucket_shift,
+    // linear probing over buckets, empty key 0
+    const uint4* hot_buckets = nullptr;
+    const uint32_t* bucket_results = nullptr;  // glibc's result bits, parallel to the bucket slots
+    uint32_t bucket_mask = 0;
+    int32_t bucket_shift = 32;
     uint32_t region_shift = 31;
     uint32_t n_regions = 0;
 };
