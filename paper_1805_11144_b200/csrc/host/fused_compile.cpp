@@ -25,6 +25,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <random>
 #include <sstream>
 #include <unordered_map>
 
@@ -55,7 +56,7 @@ class FusedImpl : public FusedPlan {
   public:
     FusedProgram prog;
     int dmax = 8, grid = 1, steps_per_launch = 0;
-    DevMem d_ens, d_conns, d_incoming, d_orphans, d_my_conns, d_values, d_probes, d_feeds, d_call, d_prof, d_work, d_xbuf;
+    DevMem d_ens, d_conns, d_incoming, d_orphans, d_my_conns, d_values, d_probes, d_feeds, d_call, d_prof, d_work, d_xbuf, d_df;
     std::string desc;
 
     FusedProgram call;  // the open call's program (begin .. step)
@@ -84,8 +85,9 @@ class FusedImpl : public FusedPlan {
             cuda_check(cudaMemsetAsync(d_prof.p, 0, (FS_COUNT + 4) * 8, stream), "profile reset");
             p.prof = d_prof.as<unsigned long long>();
         }
-        d_work.ensure(16);
+        d_work.ensure(16 + static_cast<size_t>(units) * 4);
         p.work = d_work.as<int32_t>();
+        p.done = p.work + 4;
         call = p;
     }
 
@@ -95,6 +97,7 @@ class FusedImpl : public FusedPlan {
 
     void launch(int k0, int k1, int flags, cudaStream_t stream) override {
         FusedProgram p = call;
+        p.dataflow = 0;  // stepped calls: one barrier per step (the host exchanges xhat between them)
         p.first_update = (flags & NENG_STEP_FIRST_UPDATE) ? 1 : 0;
         p.epilogue = (flags & NENG_STEP_EPILOGUE) ? 1 : 0;
         cuda_check(cudaMemsetAsync(d_work.p, 0, 8, stream), "fused work reset");
@@ -108,22 +111,28 @@ class FusedImpl : public FusedPlan {
     }
 
     void set_xhat_buffer(float* d_buf) override {
+        dataflow = false;  // a caller's buffer holds two parity slots
         prog.xbuf = d_buf;
         call.xbuf = d_buf;
     }
 
     int xstride = 0;  // parity-buffer rows per shard
+    bool dataflow = false;  // barrier-free stepping in run() (unsharded, own xhat buffer)
+    int units = 0;
 
     int64_t run(int n_steps, const float* d_feed_data, const int64_t* feed_off, const int* present, float* d_ring,
                 const int64_t* ring_off, cudaStream_t stream) override {
         begin(n_steps, d_feed_data, feed_off, present, d_ring, ring_off, stream);
         int K = steps_per_launch > 0 ? steps_per_launch : n_steps;
+        if (dataflow) K = std::max(1, std::min<int>(K, static_cast<int>((int64_t{1} << 30) / std::max(units, 1))));
         int64_t launches = 0;
         for (int k = 0; k < n_steps; k += K) {
             FusedProgram p = call;
             p.first_update = 0;
             p.epilogue = 1;
-            cuda_check(cudaMemsetAsync(d_work.p, 0, 8, stream), "fused work reset");
+            p.dataflow = dataflow ? 1 : 0;
+            cuda_check(cudaMemsetAsync(d_work.p, 0, dataflow ? 16 + static_cast<size_t>(units) * 4 : 8, stream),
+                       "fused work reset");
             cuda_check(launch_fused(p, dmax, grid, k, std::min(n_steps, k + K), stream), "fused kernel launch");
             ++launches;
         }
@@ -149,6 +158,44 @@ class FusedImpl : public FusedPlan {
     std::string describe() const override { return desc; }
     int n_probe_total = 0;
 };
+
+/// Claim order for barrier-free stepping: a permutation of the ensembles such
+/// that a source's position in step t is not within `window` (the units in
+/// flight at once, with margin) of the end when its destination's position in
+/// step t+1 comes up — the wait a unit would otherwise spend.  Random pair swaps
+/// that do not increase the number of such edges (deterministic seed).
+std::vector<int> dataflow_order(int n, const std::vector<std::vector<int>>& srcs,
+                                const std::vector<std::vector<int>>& dsts, int window) {
+    std::vector<int> order(n), pos(n);
+    for (int i = 0; i < n; ++i) order[i] = pos[i] = i;
+    const int thr = n - (window * 8 + 4) / 5;  // an edge s -> e is late when pos[s] - pos[e] > thr
+    if (n < 4 || thr <= 0) return order;
+    auto cost = [&](int x) {
+        int c = 0;
+        for (int s : srcs[x]) c += pos[s] - pos[x] > thr;
+        for (int d : dsts[x]) c += pos[x] - pos[d] > thr;
+        return c;
+    };
+    std::mt19937 rng(12345u);
+    std::uniform_int_distribution<int> pick(0, n - 1);
+    const int64_t iters = std::min<int64_t>(int64_t{40} * n, 400000);
+    for (int64_t it = 0; it < iters; ++it) {
+        const int a = pick(rng), b = pick(rng);
+        if (a == b) continue;
+        const int ea = order[a], eb = order[b];
+        const int c0 = cost(ea) + cost(eb);
+        pos[ea] = b;
+        pos[eb] = a;
+        if (cost(ea) + cost(eb) <= c0) {
+            order[a] = eb;
+            order[b] = ea;
+        } else {
+            pos[ea] = a;
+            pos[eb] = b;
+        }
+    }
+    return order;
+}
 
 bool is_full(const BuiltModel& m, const SignalRef& r) { return r.start == 0 && r.stop == m.signals[r.signal].rows(); }
 
@@ -514,6 +561,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         }
         // probes
         std::vector<FProbe> fp;
+        std::vector<int> fp_ens;  // producing ensemble of each capture (-1: a fed node)
         p.time_probe_step = p.time_probe_time = -1;
         for (size_t q = 0; q < m.probes.size(); ++q) {
             int s = m.probes[q].signal;
@@ -530,7 +578,10 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
                 // captured by the shard that produces the value (fed nodes: shard 0)
                 const bool mine = ens_of_xhat.count(s) ? (ens_of_xhat.at(s) >= ens_lo && ens_of_xhat.at(s) < ens_hi)
                                                        : R == 0;
-                if (mine) fp.push_back(pr);
+                if (mine) {
+                    fp.push_back(pr);
+                    fp_ens.push_back(ens_of_xhat.count(s) ? ens_of_xhat.at(s) : -1);
+                }
             } else if (conn_of_filt.count(s)) {
                 FConn& x = fc[conn_of_filt[s]];
                 if (x.probe_filt >= 0) fail("two probes on one filtered value");
@@ -557,6 +608,51 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             ff.push_back(x);
         }
 
+        // barrier-free stepping tables: per-ensemble waits, destination-less
+        // connections by source, xhat captures; the epilogue's connections
+        std::vector<int32_t> df_deps, df_orph, df_free, df_xp, df_dest;
+        std::vector<std::vector<int>> ens_srcs(fe.size()), ens_dsts(fe.size());
+        {
+            std::vector<std::vector<int>> orph(fe.size()), xps(fe.size());
+            for (size_t ci = 0; ci < conns.size(); ++ci) {
+                const ConnInfo& c = conns[ci];
+                const int s = ens_of_xhat.count(c.src) ? ens_of_xhat.at(c.src) : -1;
+                if (c.dst_ens >= 0) {
+                    df_dest.push_back(static_cast<int32_t>(ci));
+                    if (s >= 0) {
+                        ens_srcs[c.dst_ens].push_back(s);
+                        ens_dsts[s].push_back(c.dst_ens);
+                    }
+                } else if (s >= 0) {
+                    orph[s].push_back(static_cast<int>(ci));
+                } else {
+                    df_free.push_back(static_cast<int32_t>(ci));
+                }
+            }
+            for (size_t q = 0; q < fp.size(); ++q)
+                if (fp_ens[q] >= 0) xps[fp_ens[q]].push_back(static_cast<int>(q));
+            for (size_t e = 0; e < fe.size(); ++e) {
+                std::vector<int> pre = ens_srcs[e];
+                pre.push_back(static_cast<int>(e));
+                std::sort(pre.begin(), pre.end());
+                pre.erase(std::unique(pre.begin(), pre.end()), pre.end());
+                std::vector<int> post = ens_dsts[e];
+                std::sort(post.begin(), post.end());
+                post.erase(std::unique(post.begin(), post.end()), post.end());
+                fe[e].dep_begin = static_cast<int32_t>(df_deps.size());
+                for (int x : pre) df_deps.push_back(x << 1);
+                for (int x : post)
+                    if (!std::binary_search(pre.begin(), pre.end(), x)) df_deps.push_back((x << 1) | 1);
+                fe[e].dep_count = static_cast<int32_t>(df_deps.size()) - fe[e].dep_begin;
+                fe[e].orph_begin = static_cast<int32_t>(df_orph.size());
+                for (int c : orph[e]) df_orph.push_back(c);
+                fe[e].orph_count = static_cast<int32_t>(orph[e].size());
+                fe[e].xp_begin = static_cast<int32_t>(df_xp.size());
+                for (int q : xps[e]) df_xp.push_back(q);
+                fe[e].xp_count = static_cast<int32_t>(xps[e].size());
+            }
+        }
+
         auto upload = [](DevMem& d, const void* src, size_t bytes) {
             d.ensure(std::max<size_t>(bytes, 16));
             if (bytes) cuda_check(cudaMemcpy(d.p, src, bytes, cudaMemcpyHostToDevice), "fused H2D");
@@ -565,8 +661,9 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         upload(impl->d_conns, fc.data(), fc.size() * sizeof(FConn));
         upload(impl->d_incoming, incoming.data(), incoming.size() * sizeof(int32_t));
         upload(impl->d_orphans, orphans.data(), orphans.size() * sizeof(int32_t));
-        impl->d_xbuf.ensure(static_cast<size_t>(2) * std::max(xrows, 1) * B * sizeof(float));
-        cuda_check(cudaMemset(impl->d_xbuf.p, 0, static_cast<size_t>(2) * std::max(xrows, 1) * B * sizeof(float)),
+        // three slots: parity with a barrier per step, k % 3 barrier-free
+        impl->d_xbuf.ensure(static_cast<size_t>(3) * std::max(xrows, 1) * B * sizeof(float));
+        cuda_check(cudaMemset(impl->d_xbuf.p, 0, static_cast<size_t>(3) * std::max(xrows, 1) * B * sizeof(float)),
                    "xbuf clear");
         upload(impl->d_values, values.data(), values.size() * sizeof(float));
         upload(impl->d_probes, fp.data(), fp.size() * sizeof(FProbe));
@@ -634,10 +731,39 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         if (const char* env = std::getenv("NENG_FUSED_GRID"))  // experiments: fewer co-resident CTAs
             impl->grid = std::max(1, std::min(impl->grid, std::atoi(env)));
 
+        // barrier-free stepping (unsharded): claim order of the units
+        impl->units = (ens_hi - ens_lo) * p.groups;
+        const char* dfe = std::getenv("NENG_FUSED_DATAFLOW");
+        impl->dataflow = W == 1 && !(dfe && std::atoi(dfe) == 0);
+        {
+            const int NE = static_cast<int>(fe.size());
+            const int window = (impl->grid + p.groups - 1) / p.groups;  // ensembles in flight at once
+            std::vector<int> perm = dataflow_order(NE, ens_srcs, ens_dsts, window);
+            std::vector<int32_t> order;
+            if (W == 1)
+                for (int e : perm)
+                    for (int g = 0; g < p.groups; ++g) order.push_back(e * p.groups + g);
+            const size_t n_order = order.size(), n_deps = df_deps.size(), n_orph = df_orph.size(),
+                         n_xp = df_xp.size(), n_free = df_free.size();
+            std::vector<int32_t> blob;
+            for (auto* v : {&order, &df_deps, &df_orph, &df_xp, &df_free, &df_dest}) blob.insert(blob.end(), v->begin(), v->end());
+            upload(impl->d_df, blob.data(), blob.size() * sizeof(int32_t));
+            const int32_t* base = impl->d_df.as<int32_t>();
+            p.order = base;
+            p.deps = base + n_order;
+            p.ens_orph = p.deps + n_deps;
+            p.xprobes = p.ens_orph + n_orph;
+            p.free_orph = p.xprobes + n_xp;
+            p.n_free_orph = static_cast<int32_t>(n_free);
+            p.dest_conns = p.free_orph + n_free;
+            p.n_dest_conns = static_cast<int32_t>(df_dest.size());
+            upload(impl->d_ens, fe.data(), fe.size() * sizeof(FEns));  // with the dep / orphan / capture ranges
+        }
+
         std::ostringstream os;
         os << "fused: " << p.n_ens << " ensembles, " << p.n_conn << " connections, dmax " << impl->dmax << ", grid "
            << impl->grid << ", tiles/unit " << p.tu << ", slices " << p.slices << ", stage_dec " << p.stage_dec
-           << ", smem " << fused_smem_bytes(p, impl->dmax);
+           << ", smem " << fused_smem_bytes(p, impl->dmax) << (impl->dataflow ? ", barrier-free" : "");
         impl->desc = os.str();
         return impl;
     } catch (const Fail& f) {

@@ -34,6 +34,7 @@
 //   LIF  : lif_spike_step<float>                                         (neuron_math.hpp:55-77)
 //   xhat : payload + (0 + sum_i D[r,i]*out[i])                            (exec.cpp:226-240)
 //   acc  : payload + (0 + sum_j T[r,j]*src[j]);  f = a*state + b*acc      (exec.cpp:267-284)
+#include <algorithm>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -462,6 +463,13 @@ __device__ __forceinline__ void dq_batch(const QEnt* q, int cnt, const DqConst& 
 
 // ---- connections ----------------------------------------------------------
 
+/// The xhat buffer slot of step k: parity (two slots) with a barrier per step,
+/// k % 3 when stepping barrier-free (a slot is rewritten only after the
+/// destinations that read it have finished the step after).
+__device__ __forceinline__ int64_t xslot(const FusedProgram& p, int k) {
+    return p.dataflow ? k % 3 : k & 1;
+}
+
 /// Step-kk update of connection cn for batch column b, rows [r_lo, r_hi):
 /// acc = payload + T.src(kk) (sequential in j); f = a*state + b*acc; state = f.
 /// Returns f in f_out[r].  last: also write acc and filt to the arena.
@@ -473,7 +481,7 @@ __device__ __forceinline__ void conn_rows(const FusedProgram& p, const FConn& cn
     float* A = p.arena;
     const float* src;
     if (cn.src_xb >= 0)
-        src = p.xbuf + (static_cast<int64_t>(kk & 1) * p.xrows + cn.src_xb) * B + b;
+        src = p.xbuf + (xslot(p, kk) * p.xrows + cn.src_xb) * B + b;
     else if (cn.src_feed >= 0 && p.feed_present[cn.src_feed])
         src = p.feed_data + p.feed_off[cn.src_feed] + static_cast<int64_t>(kk) * cn.ds * B + b;
     else
@@ -514,35 +522,35 @@ __device__ __forceinline__ void conn_rows(const FusedProgram& p, const FConn& cn
     }
 }
 
-/// Grid-stride work of step kk that is not owned by a unit: connection
-/// updates (all connections in the epilogue, destination-less ones otherwise),
-/// probe captures and the clock.
+/// Work of step kk that is not owned by a unit, strided over threads
+/// [tid, nthreads): connection updates (all connections in the epilogue,
+/// destination-less ones otherwise), probe captures (captures: 0 none, 1 all,
+/// 2 all but xhat, which barrier-free units capture themselves) and the clock.
 template <int DMAX, int BT>
-__device__ void grid_step_work(const FusedProgram& p, int kk, bool all_conns, bool last) {
+__device__ void step_work(const FusedProgram& p, int kk, const int* list, int nc, int captures, bool last, int64_t tid,
+                          int64_t nthreads) {
     const int B = batch_of<BT>(p);
-    const int64_t gthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int nc = all_conns ? p.n_my_conns : p.n_orphans;
-    const int* list = all_conns ? p.my_conns : p.orphans;
     const int64_t items = static_cast<int64_t>(nc) * B;
-    for (int64_t it = gtid; it < items; it += gthreads) {
+    for (int64_t it = tid; it < items; it += nthreads) {
         const int q = static_cast<int>(it / B);
         const int b = static_cast<int>(it - static_cast<int64_t>(q) * B);
         const int c = __ldg(list + q);
         float f[DMAX];
         conn_rows<DMAX, BT>(p, p.conns[c], kk, b, 0, p.conns[c].dd, true, last, f);
     }
+    if (!captures) return;
     for (int q = 0; q < p.n_probes; ++q) {
         const FProbe& pr = p.probes[q];
+        if (captures == 2 && pr.xb_row >= 0) continue;
         const int64_t n = static_cast<int64_t>(pr.dim) * B;
         float* dst = p.ring + p.ring_off[pr.index] + static_cast<int64_t>(kk) * pr.dim * B;
         const bool fed = pr.feed_slot >= 0 && p.feed_present[pr.feed_slot];
-        for (int64_t i = gtid; i < n; i += gthreads) {
+        for (int64_t i = tid; i < n; i += nthreads) {
             const int64_t d = i / B;
             const int bb = static_cast<int>(i - d * B);
             float val;
             if (pr.xb_row >= 0)
-                val = p.xbuf[(static_cast<int64_t>(kk & 1) * p.xrows + pr.xb_row + d) * B + bb];
+                val = p.xbuf[(xslot(p, kk) * p.xrows + pr.xb_row + d) * B + bb];
             else if (fed)
                 val = p.feed_data[p.feed_off[pr.feed_slot] + static_cast<int64_t>(kk) * pr.dim * B + d * B +
                                   (pr.per_batch ? bb : 0)];
@@ -551,7 +559,7 @@ __device__ void grid_step_work(const FusedProgram& p, int kk, bool all_conns, bo
             dst[i] = val;
         }
     }
-    if (p.has_time && gtid == 0) {  // TimeUpdate (exec.cpp:300-309)
+    if (p.has_time && tid == 0) {  // TimeUpdate (exec.cpp:300-309)
         const float next = p.arena[p.step_base] + 1.0f;
         p.arena[p.step_base] = next;
         p.arena[p.time_base] = next * p.dt;
@@ -560,6 +568,31 @@ __device__ void grid_step_work(const FusedProgram& p, int kk, bool all_conns, bo
         if (p.time_probe_time >= 0)
             for (int bb = 0; bb < B; ++bb)
                 p.ring[p.ring_off[p.time_probe_time] + static_cast<int64_t>(kk) * B + bb] = next * p.dt;
+    }
+}
+
+template <int DMAX, int BT>
+__device__ void grid_step_work(const FusedProgram& p, int kk, const int* list, int nc, int captures, bool last) {
+    step_work<DMAX, BT>(p, kk, list, nc, captures, last, static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
+                        static_cast<int64_t>(gridDim.x) * blockDim.x);
+}
+
+/// write_feeds (exec.cpp:313-326) of step k into the arena, strided over
+/// threads: only the call's last step's values survive (connections read fed
+/// sources from the feed block).
+template <int BT>
+__device__ void write_feeds(const FusedProgram& p, int k, int64_t tid, int64_t nthreads) {
+    const int B = batch_of<BT>(p);
+    for (int f = 0; f < p.n_feeds; ++f) {
+        if (!p.feed_present[f]) continue;
+        const FFeed& fd = p.feeds[f];
+        const float* src = p.feed_data + p.feed_off[f] + static_cast<int64_t>(k) * fd.dim * B;
+        const int64_t n = static_cast<int64_t>(fd.dim) * fd.copies;
+        for (int64_t i = tid; i < n; i += nthreads) {
+            const int64_t d = i / fd.copies;
+            const int bb = static_cast<int>(i - d * fd.copies);
+            p.arena[fd.base + d * (fd.copies > 1 ? B : 1) + bb] = src[d * B + bb];
+        }
     }
 }
 
@@ -581,9 +614,52 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
 
 // ---- the unit ---------------------------------------------------------------
 
+// ---- barrier-free stepping (FusedProgram::dataflow) ---------------------------
+
+__device__ __forceinline__ int ld_acquire(const int* f) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(int* f, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
+
+/// Thread 0 waits until unit (ensemble ei, group g) may run step t of the
+/// launch: its sources and itself have finished step t-1, its destinations
+/// step t-2.  (The caller's __syncthreads publishes the result to the CTA.)
+__device__ __forceinline__ void df_wait(const FusedProgram& p, int ei, int g, int t) {
+    if (threadIdx.x != 0) return;
+    const int begin = p.ens[ei].dep_begin, cnt = p.ens[ei].dep_count;
+    for (int i = 0; i < cnt; ++i) {
+        const int d = __ldg(p.deps + begin + i);
+        const int need = t - (d & 1);
+        const int* f = p.done + static_cast<int64_t>((d >> 1) - p.ens_lo) * p.groups + g;
+        while (need > 0 && ld_acquire(f) < need) __nanosleep(32);
+    }
+    __threadfence();
+}
+
+/// Destination-less connections fed by ensemble ei: step-k update for the
+/// unit's batch columns, after its decode.
+template <int DMAX, int BT>
+__device__ void df_orphans(const FusedProgram& p, int ei, int g, int k, bool last) {
+    const FEns& e = p.ens[ei];
+    const int B = batch_of<BT>(p);
+    const int c0 = g * p.tu * 32, cols = min(B, c0 + p.tu * 32) - c0;
+    const int items = e.orph_count * cols;
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+        const int q = it / cols;
+        const int c = __ldg(p.ens_orph + e.orph_begin + q);
+        float f[DMAX];
+        conn_rows<DMAX, BT>(p, p.conns[c], k, c0 + it - q * cols, 0, p.conns[c].dd, true, last, f);
+    }
+}
+
 template <int DMAX, int BT, bool PROF>
 __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bool last, const Smem& S,
-                         uint32_t parity, Ticker<PROF>& tk) {
+                         uint32_t parity, Ticker<PROF>& tk, int df_pos, int df_t) {
     const int B = batch_of<BT>(p);
     const int ul = u / p.groups;
     const int g = u - ul * p.groups;
@@ -608,6 +684,16 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
         bulk_g2s(S.E, p.values + e.epad_off, eb, S.bar);
         bulk_g2s(S.bias, p.values + e.bias_off, bb, S.bar);
         if (pb) bulk_g2s(S.P, p.values + e.dec_scaled_off, pb, S.bar);
+    }
+    if (df_pos >= 0) {  // barrier-free schedule: wait for the dependencies (overlaps the staging copies)
+        df_wait(p, ei, g, df_t);
+        __syncthreads();
+        tk.tick(FS_BAR);
+        if (df_pos == 0) {  // the step's work owned by no unit (serialised: order[0] waits for itself)
+            if (last) write_feeds<BT>(p, k, threadIdx.x, blockDim.x);
+            step_work<DMAX, BT>(p, k, p.free_orph, p.n_free_orph, 2, last, threadIdx.x, blockDim.x);
+            tk.tick(FS_DEFER);
+        }
     }
 
     // 1. connection updates of step k-1 (destination side) and the input sum, plan order
@@ -891,14 +977,23 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
                 }
             }
             if (valid) {
-                float* xo = p.xbuf + (static_cast<int64_t>(k & 1) * p.xrows + e.xb_row + r0) * B + b;
+                float* xo = p.xbuf + (xslot(p, k) * p.xrows + e.xb_row + r0) * B + b;
 #pragma unroll
                 for (int q = 0; q < DMAX; ++q) {
                     if (q < rn) {
                         const float xv = __ldg(p.values + e.xhat_init_off + r0 + q) + a[q];
                         xo[static_cast<int64_t>(q) * B] = xv;
                         if (last) A[e.xhat_base + static_cast<int64_t>(r0 + q) * B + b] = xv;
+                        a[q] = xv;
                     }
+                }
+                // barrier-free stepping captures xhat probes here (else grid_step_work does)
+                for (int c = 0; p.dataflow && c < e.xp_count; ++c) {
+                    const FProbe& pr = p.probes[__ldg(p.xprobes + e.xp_begin + c)];
+                    float* dst = p.ring + p.ring_off[pr.index] + (static_cast<int64_t>(k) * pr.dim + r0) * B + b;
+#pragma unroll
+                    for (int q = 0; q < DMAX; ++q)
+                        if (q < rn) dst[static_cast<int64_t>(q) * B] = a[q];
                 }
             }
         }
@@ -908,9 +1003,20 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
                 A[e.out_base + static_cast<int64_t>(i) * B + b] = (words[i] >> lane) & 1u ? e.amp_dt : 0.0f;
     }
     tk.tick(FS_DECODE);
+    if (df_pos >= 0) {  // barrier-free schedule: destination-less connections, then publish the step
+        __syncthreads();
+        if (e.orph_count) {
+            df_orphans<DMAX, BT>(p, ei, g, k, last);
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            __threadfence();
+            st_release(p.done + u, df_t + 1);
+        }
+    }
 }
 
-template <int DMAX, int BT, bool PROF>
+template <int DMAX, int BT, bool PROF, bool DF>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) fused_run_kernel(const __grid_constant__ FusedProgram p, int k_begin, int k_end) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(128) uint32_t smem[];
@@ -930,79 +1036,110 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fused_run_kernel(const _
     Ticker<PROF> tk;
     tk.start();
 
-    for (int k = k_begin; k < k_end; ++k) {
-        const bool last = k == p.call_steps - 1;
-        if (gtid == 0) p.work[(k + 1) & 1] = 0;  // last used by step k-1; next used by step k+1
-        // write_feeds (exec.cpp:313-326) into the arena: only the last step's
-        // values survive a call; connections read fed sources from the feed block
-        for (int f = 0; last && f < p.n_feeds; ++f) {
-            if (!p.feed_present[f]) continue;
-            const FFeed& fd = p.feeds[f];
-            const float* src = p.feed_data + p.feed_off[f] + static_cast<int64_t>(k) * fd.dim * B;
-            const int64_t n = static_cast<int64_t>(fd.dim) * fd.copies;
-            for (int64_t i = gtid; i < n; i += gthreads) {
-                const int64_t d = i / fd.copies;
-                const int bb = static_cast<int>(i - d * fd.copies);
-                p.arena[fd.base + d * (fd.copies > 1 ? B : 1) + bb] = src[d * B + bb];
+    if constexpr (!DF) {
+        // one grid barrier per step: the units of step k are claimed from work[k & 1]
+        for (int k = k_begin; k < k_end; ++k) {
+            const bool last = k == p.call_steps - 1;
+            if (gtid == 0) p.work[(k + 1) & 1] = 0;  // last used by step k-1; next used by step k+1
+            if (last) write_feeds<BT>(p, k, gtid, gthreads);
+            const bool upd = k > k_begin || p.first_update;
+            if (upd) grid_step_work<DMAX, BT>(p, k - 1, p.orphans, p.n_orphans, 1, false);
+            tk.tick(FS_DEFER);
+            int* work = p.work + (k & 1);
+            for (;;) {
+                if (threadIdx.x == 0) *S.cur = atomicAdd(work, 1);
+                __syncthreads();
+                const int u = *S.cur;
+                __syncthreads();  // every thread has read cur before thread 0 claims again
+                tk.tick(FS_QUEUE);  // (profile: the unit barrier and claim)
+                if (u >= units) break;  // uniform
+                run_unit<DMAX, BT, PROF>(p, u, k, upd, last, S, parity, tk, -1, 0);
+                parity ^= 1u;
+                __syncthreads();  // staging buffers, words and queues are reused by the next unit
             }
+            grid_sync(grid);
+            tk.tick(FS_BAR);
         }
-        const bool upd = k > k_begin || p.first_update;
-        if (upd) grid_step_work<DMAX, BT>(p, k - 1, false, false);
-        tk.tick(FS_DEFER);
-        int* work = p.work + (k & 1);
+        // epilogue: connection updates, captures and clock of the launch's last step
+        if (p.epilogue)
+            grid_step_work<DMAX, BT>(p, k_end - 1, p.my_conns, p.n_my_conns, 1, k_end - 1 == p.call_steps - 1);
+    } else {
+        // barrier-free: position gi = t * units + pos of one launch-wide claim
+        // counter runs unit order[pos] of step k_begin + t once its
+        // dependencies are done; the only grid barrier precedes the epilogue
+        const int total = units * (k_end - k_begin);
         for (;;) {
-            if (threadIdx.x == 0) *S.cur = atomicAdd(work, 1);
+            if (threadIdx.x == 0) *S.cur = atomicAdd(p.work, 1);
             __syncthreads();
-            const int u = *S.cur;
+            const int gi = *S.cur;
             __syncthreads();  // every thread has read cur before thread 0 claims again
-            tk.tick(FS_QUEUE);  // (profile: the unit barrier and claim)
-            if (u >= units) break;  // uniform
-            run_unit<DMAX, BT, PROF>(p, u, k, upd, last, S, parity, tk);
+            tk.tick(FS_QUEUE);
+            if (gi >= total) break;  // uniform
+            const int t = gi / units, pos = gi - t * units;
+            const int u = __ldg(p.order + pos);
+            const int k = k_begin + t;
+            run_unit<DMAX, BT, PROF>(p, u, k, t > 0 || p.first_update, k == p.call_steps - 1, S, parity, tk, pos, t);
             parity ^= 1u;
             __syncthreads();  // staging buffers, words and queues are reused by the next unit
         }
         grid_sync(grid);
         tk.tick(FS_BAR);
+        // epilogue: the step k_end-1 updates of connections into ensembles (the
+        // units captured their xhat and updated their destination-less connections)
+        if (p.epilogue)
+            grid_step_work<DMAX, BT>(p, k_end - 1, p.dest_conns, p.n_dest_conns, 0, k_end - 1 == p.call_steps - 1);
     }
-    // epilogue: connection updates, captures and clock of the launch's last step
-    if (p.epilogue) grid_step_work<DMAX, BT>(p, k_end - 1, true, k_end - 1 == p.call_steps - 1);
     tk.tick(FS_EPI);
     tk.flush(p.prof);
 }
 
-template <int DMAX, int BT, bool PROF>
-cudaError_t launch_t(const FusedProgram& p, int grid, int k0, int k1, cudaStream_t stream) {
+template <int DMAX, int BT, bool PROF, bool DF>
+cudaError_t launch_k(const FusedProgram& p, int grid, int k0, int k1, cudaStream_t stream) {
     size_t sm = smem_bytes<DMAX>(p);
     if (sm > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(fused_run_kernel<DMAX, BT, PROF>,
+        cudaError_t e = cudaFuncSetAttribute(fused_run_kernel<DMAX, BT, PROF, DF>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
         if (e != cudaSuccess) return e;
     }
     FusedProgram prog = p;
     void* args[] = {&prog, &k0, &k1};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fused_run_kernel<DMAX, BT, PROF>), dim3(grid),
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fused_run_kernel<DMAX, BT, PROF, DF>), dim3(grid),
                                        dim3(kThreads), args, sm, stream);
+}
+
+template <int DMAX, int BT, bool PROF>
+cudaError_t launch_t(const FusedProgram& p, int grid, int k0, int k1, cudaStream_t stream) {
+    return p.dataflow ? launch_k<DMAX, BT, PROF, true>(p, grid, k0, k1, stream)
+                      : launch_k<DMAX, BT, PROF, false>(p, grid, k0, k1, stream);
+}
+
+template <int DMAX, int BT, bool PROF, bool DF>
+int per_sm_k(size_t sm) {
+    if (sm > 48 * 1024)
+        cudaFuncSetAttribute(fused_run_kernel<DMAX, BT, PROF, DF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sm));
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fused_run_kernel<DMAX, BT, PROF, DF>, kThreads, sm);
+    return n;
 }
 
 template <int DMAX, int BT>
 int max_grid_t(const FusedProgram& p, int device) {
     size_t sm = smem_bytes<DMAX>(p);
     if (sm > 227 * 1024) return 0;
-    if (sm > 48 * 1024) {
-        cudaFuncSetAttribute(fused_run_kernel<DMAX, BT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(sm));
-        cudaFuncSetAttribute(fused_run_kernel<DMAX, BT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(sm));
-    }
-    int per_sm = 0, per_sm_prof = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_run_kernel<DMAX, BT, false>, kThreads, sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_prof, fused_run_kernel<DMAX, BT, true>, kThreads, sm);
+    const int per_sm = std::min(std::min(per_sm_k<DMAX, BT, false, false>(sm), per_sm_k<DMAX, BT, true, false>(sm)),
+                                std::min(per_sm_k<DMAX, BT, false, true>(sm), per_sm_k<DMAX, BT, true, true>(sm)));
+    int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    return (per_sm < per_sm_prof ? per_sm : per_sm_prof) * sms;
+    return per_sm * sms;
 }
 
 // Batch widths with a stride-specialised kernel (others run the runtime-stride one).
+#ifdef NENG_FUSED_DEBUG_BUILD  // quick experiment builds: generic batch width only
+#define NENG_FUSED_BATCHES(X)
+#else
 #define NENG_FUSED_BATCHES(X) X(32) X(256)
+#endif
 
 template <int DMAX, bool PROF>
 cudaError_t launch_d(const FusedProgram& p, int grid, int k0, int k1, cudaStream_t stream) {
@@ -1038,9 +1175,13 @@ size_t fused_smem_bytes(const FusedProgram& p, int dmax) {
 cudaError_t launch_fused(const FusedProgram& p, int dmax, int grid, int k0, int k1, cudaStream_t stream) {
     const bool prof = p.prof != nullptr;
     switch (dmax) {
+#ifdef NENG_FUSED_DEBUG_BUILD
+        case 8: return prof ? cudaErrorNotSupported : launch_d<8, false>(p, grid, k0, k1, stream);
+#else
         case 8: return prof ? launch_d<8, true>(p, grid, k0, k1, stream) : launch_d<8, false>(p, grid, k0, k1, stream);
         case 16: return prof ? launch_d<16, true>(p, grid, k0, k1, stream) : launch_d<16, false>(p, grid, k0, k1, stream);
         case 32: return prof ? launch_d<32, true>(p, grid, k0, k1, stream) : launch_d<32, false>(p, grid, k0, k1, stream);
+#endif
     }
     return cudaErrorInvalidValue;
 }
@@ -1048,8 +1189,10 @@ cudaError_t launch_fused(const FusedProgram& p, int dmax, int grid, int k0, int 
 int fused_max_grid(const FusedProgram& p, int dmax, int device) {
     switch (dmax) {
         case 8: return max_grid_d<8>(p, device);
+#ifndef NENG_FUSED_DEBUG_BUILD
         case 16: return max_grid_d<16>(p, device);
         case 32: return max_grid_d<32>(p, device);
+#endif
     }
     return 0;
 }

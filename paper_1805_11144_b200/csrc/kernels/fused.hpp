@@ -13,7 +13,8 @@
 //      refractory period: expm1) leave the sweep through warp queues and are
 //      resolved 32 at a time;
 //   3. decodes xhat = Reset payload + sum over spiking i (ascending) of
-//      D[r,i]*(amp/dt) into the step-parity buffer xbuf[k & 1].
+//      D[r,i]*(amp/dt) into the step-parity buffer xbuf[k & 1] (xbuf[k % 3]
+//      when stepping barrier-free, see FusedProgram::dataflow).
 // The update of step k-1 for connections without a destination ensemble, the
 // probe captures of step k-1 and the clock run at the start of step k; the
 // launch's last step is completed by an epilogue after a final barrier.
@@ -47,6 +48,10 @@ struct FEns {
     float amp_dt;  // amplitude / dt (the spike value, exec: amplitude / dt)
     float em_dt;   // glibc expm1f(-dt / tau_rc): the refractory-free step
     double inv_tau_rc;  // 1 / (double)tau_rc
+    // barrier-free stepping (FusedProgram::dataflow): index ranges into deps / ens_orph / xprobes
+    int32_t dep_begin, dep_count;    // (ensemble << 1) | lag: wait for done >= t - lag
+    int32_t orph_begin, orph_count;  // destination-less connections this ensemble feeds
+    int32_t xp_begin, xp_count;      // captures of this ensemble's xhat
 };
 
 struct FConn {
@@ -109,8 +114,22 @@ struct FusedProgram {
     // optional section timers (NENG_FUSED_PROFILE=1): per-CTA ns summed over CTAs
     unsigned long long* prof = nullptr;
     int32_t* work = nullptr;  // two unit counters (step parity), zero at launch
-    void* dq = nullptr;       // per-warp doubt lists (16-B entries), resolved after each unit's decode
-    int32_t dq_cap = 0;       // entries per warp
+    // barrier-free stepping (unsharded runs): unit (e, g) of step t waits for
+    // done[s, g] >= t of its sources and itself and done[d, g] >= t - 1 of its
+    // destinations (xbuf is triple-buffered: slot k % 3), then publishes
+    // done[e, g] = t + 1.  Units are claimed in `order` (a permutation that keeps
+    // a unit's sources away from the end of the previous step), so there is no
+    // grid barrier and no end-of-step tail; one barrier before the epilogue.
+    int32_t dataflow = 0;
+    int32_t* done = nullptr;            // per unit (local index), zero at launch
+    const int32_t* order = nullptr;     // claim position -> unit
+    const int32_t* deps = nullptr;      // FEns::dep_*
+    const int32_t* ens_orph = nullptr;  // FEns::orph_*
+    const int32_t* xprobes = nullptr;   // FEns::xp_*: indices into probes
+    const int32_t* free_orph = nullptr;   // destination-less connections from fed / constant sources
+    int32_t n_free_orph = 0;
+    const int32_t* dest_conns = nullptr;  // connections into an ensemble (the epilogue's)
+    int32_t n_dest_conns = 0;
 };
 
 enum FusedSection { FS_DEFER, FS_IN, FS_SWEEP, FS_QUEUE, FS_FIX, FS_DECODE, FS_BAR, FS_EPI, FS_COUNT };

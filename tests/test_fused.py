@@ -195,3 +195,51 @@ def test_hard_driven_network_bit_exact_full_state():
     ref = refapi.RefEngine(pm, w.batch)
     assert_bitexact(gpu.run(w.steps, feeds), ref.run(w.steps, feeds), "hard driven")
     full_state_equal(gpu, ref, pm.model, w.batch, "hard driven")
+
+
+def probe_rich_network(seed=11, batch=40, steps=26):
+    """Small ring network with every capture and connection kind the fused
+    pipeline owns outside the units: a destination-less connection from an
+    ensemble and one from a fed node (filt and state probes), two probes on one
+    xhat, a fed-node probe and the clock's step/time probes."""
+    nb = networks.NetBuilder(seed)
+    rng = np.random.default_rng(seed)
+    ens = [nb.ensemble(48, 3) for _ in range(6)]
+    xs = [nb.decoded(e, rng.normal(0.0, 0.2, size=(3, 48))) for e in ens]
+    for i in range(6):
+        for j in (1, 3):
+            nb.connect(xs[i], ens[(i + j) % 6].in_, rng.normal(0.0, 0.5, size=(3, 3)), synapse=0.01)
+    node, u = nb.feedable_node(3, np.zeros(3))
+    nb.connect(u, ens[0].in_, None, synapse=0.01)
+    node2, u2 = nb.feedable_node(2, np.full(2, 0.25))
+    po = nb.connect(xs[2], None, rng.normal(size=(2, 3)), synapse=0.02)
+    pf = nb.connect(u2, None, None, synapse=0.005)
+    nb.probe(po["filtered"], "orphan.filt")
+    nb.probe(po["state"], "orphan.state")
+    nb.probe(pf["filtered"], "fed_orphan.filt")
+    nb.probe(xs[4], "x4a")
+    nb.probe(xs[4], "x4b")
+    nb.probe(u, "feed")
+    nb.probe(0, "step")
+    nb.probe(1, "time")
+    feeds = {node: rng.standard_normal((batch, steps, 3)), node2: rng.standard_normal((batch, steps, 2))}
+    return networks.Workload("probe_rich", nb.m, batch, steps, feeds, 6 * 48)
+
+
+@pytest.mark.parametrize("dataflow", ["1", "0"])
+def test_captures_and_orphans_both_schedules(dataflow, monkeypatch):
+    # barrier-free stepping (default) and one barrier per step: captures, orphan
+    # connections, the clock and call boundaries (second call without node2's feed)
+    monkeypatch.setenv("NENG_FUSED_DATAFLOW", dataflow)
+    w = probe_rich_network()
+    pm = passes.run_passes(w.model)
+    node2 = max(w.feeds)
+    calls = [(11, step_slice(w.feeds, 0, 11)),
+             (15, {k: v for k, v in step_slice(w.feeds, 11, 15).items() if k != node2})]
+    for spl in (0, 4):
+        gpu = GpuEngine(pm, w.batch, steps_per_launch=spl)
+        assert gpu.mode() == MODE_FUSED
+        ref = refapi.RefEngine(pm, w.batch)
+        for i, (n, f) in enumerate(calls):
+            assert_bitexact(gpu.run(n, f), ref.run(n, f), f"dataflow={dataflow} spl={spl} call {i}")
+            full_state_equal(gpu, ref, pm.model, w.batch, f"dataflow={dataflow} spl={spl} call {i}")
