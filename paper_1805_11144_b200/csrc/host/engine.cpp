@@ -6,6 +6,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -774,18 +775,25 @@ void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probe
             slots.push_back(f);
             per_step += static_cast<int64_t>(feeds_[f].dim) * B;
         }
-    int cs = n_steps;
-    if (fused_ && per_step > 0) cs = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(n_steps, (int64_t{1} << 23) / per_step)));
-    const int nbuf = cs < n_steps ? 2 : 1;
+    // chunk sizes grow geometrically from a small first chunk (the only staging
+    // not overlapped with the kernel) to the largest staging buffer
+    int cs = n_steps, cs0 = n_steps;
+    if (fused_ && per_step > 0) {
+        cs = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(n_steps, (int64_t{1} << 24) / per_step)));
+        cs0 = std::max(1, std::min(cs, 4));
+    }
+    const int nbuf = cs0 < n_steps ? 2 : 1;
     feed_buf_.ensure(static_cast<size_t>(std::max<int64_t>(feed_floats, 1)) * sizeof(float));
     const size_t chunk_floats = static_cast<size_t>(std::max<int64_t>(per_step * cs, 1));
     feed_stage_.ensure(chunk_floats * nbuf * sizeof(float));
     feed_raw_.ensure(chunk_floats * nbuf * sizeof(float));
-    feed_meta_.ensure((slots.size() * 20 + 16) * nbuf);
+    const size_t meta_stride = (slots.size() * 20 + 16 + 15) / 16 * 16;  // 8-B aligned offsets in each half
+    feed_meta_.ensure(meta_stride * nbuf);
     if (!feed_events_[0]) {
         cuda_check(cudaEventCreateWithFlags(&feed_events_[0], cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&feed_events_[1], cudaEventDisableTiming), "cudaEventCreate");
     }
+    double t_conv = 0.0;
     auto stage_chunk = [&](int c0, int c1, int buf) {
         if (slots.empty()) return;
         const int n = c1 - c0;
@@ -814,6 +822,7 @@ void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probe
                 for (int64_t i = 0; i < len; ++i) out[i] = static_cast<float>(in[i]);
             }
         };
+        const auto tc = std::chrono::steady_clock::now();
         const int64_t nt = std::min<int64_t>(rows, std::max(1u, std::thread::hardware_concurrency()));
         if (nt <= 1 || at < (int64_t{1} << 20)) {
             work(0, rows);
@@ -822,7 +831,8 @@ void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probe
             for (int64_t t = 0; t < nt; ++t) pool.emplace_back(work, rows * t / nt, rows * (t + 1) / nt);
             for (auto& th : pool) th.join();
         }
-        char* meta = feed_meta_.as<char>() + (slots.size() * 20 + 16) * buf;
+        t_conv += std::chrono::duration<double>(std::chrono::steady_clock::now() - tc).count();
+        char* meta = feed_meta_.as<char>() + meta_stride * buf;
         cuda_check(cudaMemcpyAsync(raw, stage, at * sizeof(float), cudaMemcpyHostToDevice, stream_), "feed H2D");
         cuda_check(cudaMemcpyAsync(meta, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice, stream_), "feed meta");
         cuda_check(cudaMemcpyAsync(meta + offs.size() * 8, cols.data(), cols.size() * 4, cudaMemcpyHostToDevice,
@@ -835,13 +845,19 @@ void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probe
                                          static_cast<int>(slots.size()), max_cols, B, stream_),
                    "feed transpose");
     };
-    if (fused_ && cs < n_steps) {
+    const bool tprof = std::getenv("NENG_RUN_PROFILE") != nullptr;  // host-side phase times (stderr)
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    const auto t_start = now();
+    double t_stage = 0.0;
+    if (fused_ && cs0 < n_steps) {
         fused_->begin(n_steps, feed_buf_.as<float>(), full_off.data(), present.data(), ring_.as<float>(),
                       ring_off.data(), stream_);
         last_launches_ = 0;
-        for (int c0 = 0, i = 0; c0 < n_steps; c0 += cs, ++i) {
-            const int c1 = std::min(n_steps, c0 + cs);
+        for (int c0 = 0, i = 0, n = cs0; c0 < n_steps; c0 += n, n = std::min(cs, 2 * n), ++i) {
+            const int c1 = std::min(n_steps, c0 + n);
+            const auto t0 = now();
             stage_chunk(c0, c1, i & 1);
+            t_stage += std::chrono::duration<double>(now() - t0).count();
             fused_->launch(c0, c1, NENG_STEP_EPILOGUE, stream_);
             ++last_launches_;
         }
@@ -850,6 +866,16 @@ void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probe
         launch_steps(n_steps, feed_buf_.as<float>(), present, ring_.as<float>(), stream_);
     }
 
+    const auto t_issued = now();
+    if (tprof) {
+        cuda_check(cudaStreamSynchronize(stream_), "run");
+        std::fprintf(stderr,
+                     "[run profile] %d steps in %lld launches (chunks %d..%d): staging %.1f ms (conversion %.1f), issue "
+                     "%.1f ms, device done %.1f ms\n",
+                     n_steps, static_cast<long long>(last_launches_), cs0, cs, t_stage * 1e3, t_conv * 1e3,
+                     std::chrono::duration<double>(t_issued - t_start).count() * 1e3,
+                     std::chrono::duration<double>(now() - t_start).count() * 1e3);
+    }
     if (ring_floats) {
         // ring [probe][step][dim][B] -> [probe][B][step][dim], D2H, widen to f64
         std::vector<int64_t> off(probes_.size());
@@ -883,6 +909,8 @@ void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probe
     } else {
         cuda_check(cudaStreamSynchronize(stream_), "run");
     }
+    if (tprof)
+        std::fprintf(stderr, "[run profile] total %.1f ms\n", std::chrono::duration<double>(now() - t_start).count() * 1e3);
     steps_done_ += n_steps;
 }
 

@@ -1135,8 +1135,8 @@ int max_grid_t(const FusedProgram& p, int device) {
 }
 
 // Batch widths with a stride-specialised kernel (others run the runtime-stride one).
-#ifdef NENG_FUSED_DEBUG_BUILD  // quick experiment builds: generic batch width only
-#define NENG_FUSED_BATCHES(X)
+#ifdef NENG_FUSED_DEBUG_BUILD  // quick experiment builds: DMAX 8, the bench's batch width and the generic one
+#define NENG_FUSED_BATCHES(X) X(256)
 #else
 #define NENG_FUSED_BATCHES(X) X(32) X(256)
 #endif
