@@ -33,11 +33,11 @@ def main():
             out[k] = (vals[i], units[i])
             print(f"{k:70s} {vals[i]:>20s} {units[i]}")
     stalls = [(h, vals[i]) for i, h in enumerate(hdr)
-              if h.startswith("smsp__average_warp_latency_issue_stalled") and h.endswith(".ratio")]
+              if h.startswith("smsp__average_warps_issue_stalled") and h.endswith("_per_issue_active.ratio")]
     stalls = sorted(((float(v.replace(",", "")), h) for h, v in stalls if v not in ("", "n/a")), reverse=True)[:8]
     print("top stall reasons (avg cycles per issued instruction):")
     for v, h in stalls:
-        print(f"   {h.replace('smsp__average_warp_latency_issue_stalled_', ''):50s} {v:.2f}")
+        print(f"   {h.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', ''):50s} {v:.2f}")
     sass = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "source", "--csv", "--print-source=sass"))))
     h = sass[1]
     data = sass[2:]
