@@ -227,6 +227,16 @@ neng_status neng_gpu_reset(neng_engine* e);
 neng_status neng_gpu_read_signal(const neng_engine* e, int32_t signal, int32_t batch_index,
                                  double* out, int64_t capacity, int64_t* n_out);
 
+/* Probe export of the last neng_gpu_run call, replacing the reference's
+ * write_probe_binary / write_probe_csv on the ProbeOutput that run returned
+ * (export.hpp:17-25, export.cpp:53-101): the traces come from the engine's
+ * device-transposed probe block, in key order, byte-identical to the
+ * reference's output.  RunError before the first run. */
+neng_status neng_gpu_probe_dump_size(const neng_engine* e, int64_t* bytes);           /* NENG1 size */
+neng_status neng_gpu_probe_dump(const neng_engine* e, void* out, int64_t capacity);   /* NENG1 bytes */
+neng_status neng_gpu_write_probe_binary(const neng_engine* e, const char* path);
+neng_status neng_gpu_write_probe_csv(const neng_engine* e, const char* path, double dt);
+
 neng_status neng_gpu_buffer_storage(const neng_engine* e, int32_t buffer, int32_t* mode_out);
 int32_t neng_gpu_batch(const neng_engine* e);
 int32_t neng_gpu_unroll(const neng_engine* e);

@@ -15,6 +15,8 @@
 //   batch() / unroll() / steps_completed() / planned()  same   (exec.hpp:36-39)
 //   StorageMode buffer_storage(int buffer)              same   (exec.hpp:41-43)
 //   std::vector<double> read_signal(SignalId, int)      same   (exec.cpp:368-377)
+//   write_probe_binary/csv(path, run(...))              write_probe_binary/csv(path[, dt])
+//                                                       of the last run (export.hpp:17-25)
 //
 // Errors come back as the reference's own exception types (ir.hpp:15-25):
 // the C status codes map 1:1 onto StructuralError / BuildError / RunError;
@@ -113,6 +115,23 @@ class GpuEngine {
 
     /// NENG_MODE_FUSED or NENG_MODE_GENERIC: which executor the model compiled to.
     int mode() const { return neng_gpu_mode(engine_.get()); }
+
+    /// write_probe_binary / write_probe_csv (export.hpp:17-25) of the traces the
+    /// last run() returned, written from the engine's own probe block: the same
+    /// bytes as neng::write_probe_binary(path, run(...)) / write_probe_csv.
+    void write_probe_binary(const std::string& path) const {
+        check(neng_gpu_write_probe_binary(engine_.get(), path.c_str()));
+    }
+    void write_probe_csv(const std::string& path, double dt) const {
+        check(neng_gpu_write_probe_csv(engine_.get(), path.c_str(), dt));
+    }
+    std::vector<char> probe_dump() const {
+        int64_t n = 0;
+        check(neng_gpu_probe_dump_size(engine_.get(), &n));
+        std::vector<char> out(static_cast<size_t>(n));
+        check(neng_gpu_probe_dump(engine_.get(), out.data(), n));
+        return out;
+    }
 
   private:
     struct Destroy {

@@ -20,6 +20,7 @@
 
 #include "neng_gpu.h"
 #include "nengine/exec.hpp"
+#include "nengine/export.hpp"
 #include "nengine/ir.hpp"
 #include "nengine/passes.hpp"
 #include "nengine/reference.hpp"
@@ -209,6 +210,7 @@ struct nref_planned {
 struct nref_engine {
     std::unique_ptr<neng::EngineCore<float>> f32;
     std::unique_ptr<neng::EngineCore<double>> f64;
+    neng::ProbeOutput last;  // the last run's traces (for the export checks)
 };
 
 extern "C" {
@@ -362,11 +364,22 @@ neng_status nref_engine_run(nref_engine* e, int32_t n_steps, int32_t n_feeds,
         if (e->f32) {
             neng::ProbeOutput out = e->f32->run(n_steps, fd);
             if (probes_out) write_probes(e->f32->planned().model, out, probes_out);
+            e->last = std::move(out);
         } else {
             neng::ProbeOutput out = e->f64->run(n_steps, fd);
             if (probes_out) write_probes(e->f64->planned().model, out, probes_out);
+            e->last = std::move(out);
         }
     });
+}
+
+/* the reference's own write_probe_binary / write_probe_csv (export.cpp) of the last run */
+neng_status nref_engine_write_probe_binary(const nref_engine* e, const char* path) {
+    return guarded([&] { neng::write_probe_binary(std::string(path), e->last); });
+}
+
+neng_status nref_engine_write_probe_csv(const nref_engine* e, const char* path, double dt) {
+    return guarded([&] { neng::write_probe_csv(std::string(path), e->last, dt); });
 }
 
 neng_status nref_engine_reset(nref_engine* e) {

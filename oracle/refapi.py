@@ -182,6 +182,18 @@ class RefEngine:
         _check(lib, lib.nref_engine_run(C.c_void_p(self.h), n_steps, nf, fv, out.ctypes.data_as(_abi.f64p)))
         return _abi.split_probes(self.model, out, self._batch, n_steps)
 
+    def write_probe_binary(self, path: str):
+        """The reference's write_probe_binary (export.cpp) of the last run's traces."""
+        lib = ref_lib()
+        lib.nref_engine_write_probe_binary.argtypes = [C.c_void_p, C.c_char_p]
+        _check(lib, lib.nref_engine_write_probe_binary(C.c_void_p(self.h), os.fsencode(path)))
+
+    def write_probe_csv(self, path: str, dt: float):
+        """The reference's write_probe_csv (export.cpp) of the last run's traces."""
+        lib = ref_lib()
+        lib.nref_engine_write_probe_csv.argtypes = [C.c_void_p, C.c_char_p, C.c_double]
+        _check(lib, lib.nref_engine_write_probe_csv(C.c_void_p(self.h), os.fsencode(path), dt))
+
     def reset(self):
         _check(ref_lib(), ref_lib().nref_engine_reset(C.c_void_p(self.h)))
 

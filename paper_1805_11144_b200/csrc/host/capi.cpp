@@ -2,9 +2,11 @@
 // catches C++ exceptions and maps them 1:1 onto status codes (the reference's
 // StructuralError/BuildError/RunError, ir.hpp:15-25) with the message kept in
 // a thread-local (neng_last_error) and on the engine (neng_gpu_last_error).
+#include <cstdio>
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "engine.hpp"
 #include "neng_gpu.h"
@@ -114,6 +116,43 @@ neng_status neng_gpu_synchronize(neng_engine* e) {
 neng_status neng_gpu_reset(neng_engine* e) {
     if (!e) return NENG_INVALID_ARGUMENT;
     return guarded(&e->impl, [&] { e->impl.reset(); });
+}
+
+neng_status neng_gpu_probe_dump_size(const neng_engine* e, int64_t* bytes) {
+    if (!e || !bytes) return NENG_INVALID_ARGUMENT;
+    auto* ee = const_cast<neng_engine*>(e);
+    return guarded(&ee->impl, [&] { *bytes = e->impl.probe_dump_bytes(); });
+}
+
+neng_status neng_gpu_probe_dump(const neng_engine* e, void* out, int64_t capacity) {
+    if (!e || !out) return NENG_INVALID_ARGUMENT;
+    auto* ee = const_cast<neng_engine*>(e);
+    return guarded(&ee->impl, [&] { e->impl.probe_dump(static_cast<char*>(out), capacity); });
+}
+
+neng_status neng_gpu_write_probe_binary(const neng_engine* e, const char* path) {
+    if (!e || !path) return NENG_INVALID_ARGUMENT;
+    auto* ee = const_cast<neng_engine*>(e);
+    return guarded(&ee->impl, [&] {
+        std::vector<char> buf(static_cast<size_t>(e->impl.probe_dump_bytes()));
+        e->impl.probe_dump(buf.data(), static_cast<int64_t>(buf.size()));
+        std::FILE* f = std::fopen(path, "wb");
+        if (!f) throw nengb::RunError(std::string("cannot open '") + path + "' for writing");
+        const size_t n = std::fwrite(buf.data(), 1, buf.size(), f);
+        if (std::fclose(f) != 0 || n != buf.size()) throw nengb::RunError(std::string("failed writing '") + path + "'");
+    });
+}
+
+neng_status neng_gpu_write_probe_csv(const neng_engine* e, const char* path, double dt) {
+    if (!e || !path) return NENG_INVALID_ARGUMENT;
+    auto* ee = const_cast<neng_engine*>(e);
+    return guarded(&ee->impl, [&] {
+        const std::string text = e->impl.probe_csv(dt);
+        std::FILE* f = std::fopen(path, "wb");
+        if (!f) throw nengb::RunError(std::string("cannot open '") + path + "' for writing");
+        const size_t n = std::fwrite(text.data(), 1, text.size(), f);
+        if (std::fclose(f) != 0 || n != text.size()) throw nengb::RunError(std::string("failed writing '") + path + "'");
+    });
 }
 
 neng_status neng_gpu_read_signal(const neng_engine* e, int32_t signal, int32_t batch_index, double* out,

@@ -912,6 +912,109 @@ void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probe
     if (tprof)
         std::fprintf(stderr, "[run profile] total %.1f ms\n", std::chrono::duration<double>(now() - t_start).count() * 1e3);
     steps_done_ += n_steps;
+    last_run_steps_ = n_steps;
+}
+
+// ---- probe export (export.cpp:53-101) from the last run's transposed probe block ----
+
+namespace {
+/// The traces ProbeOutput holds: one per key in key order (std::map); with a
+/// key registered twice capture_probes leaves the last binding's values.
+std::vector<int> export_order(const PlannedModel& pm) {
+    std::map<int, int> last;
+    for (size_t i = 0; i < pm.model.probes.size(); ++i) last[pm.model.probes[i].key] = static_cast<int>(i);
+    std::vector<int> order;
+    for (auto [k, i] : last) order.push_back(i);
+    return order;
+}
+}  // namespace
+
+int64_t Engine::probe_dump_bytes() const {
+    if (last_run_steps_ <= 0) throw RunError("no probe traces: run() has not been called");
+    int64_t n = 5 + 1 + 4;
+    for (int i : export_order(pm_)) n += 16 + int64_t{8} * batch_ * last_run_steps_ * probe_dim(i);
+    return n;
+}
+
+void Engine::probe_dump(char* out, int64_t capacity) const {
+    const int64_t need = probe_dump_bytes();
+    if (capacity < need) throw InvalidArgument("probe dump: output capacity too small");
+    std::vector<int64_t> at(pm_.model.probes.size());  // float offset of probe i in the block
+    int64_t o = 0;
+    for (size_t i = 0; i < at.size(); ++i) {
+        at[i] = o;
+        o += int64_t{1} * batch_ * last_run_steps_ * probe_dim(static_cast<int>(i));
+    }
+    const float* blk = probe_stage_.as<float>();
+    char* p = out;
+    auto put = [&](const void* v, size_t n) {
+        std::memcpy(p, v, n);
+        p += n;
+    };
+    put("NENG1", 5);
+    const uint8_t width = 8;
+    put(&width, 1);
+    const std::vector<int> order = export_order(pm_);
+    const uint32_t count = static_cast<uint32_t>(order.size());
+    put(&count, 4);
+    for (int i : order) {
+        const int32_t hdr[4] = {pm_.model.probes[i].key, batch_, last_run_steps_, probe_dim(i)};
+        put(hdr, sizeof hdr);
+        const int64_t n = int64_t{1} * batch_ * last_run_steps_ * probe_dim(i);  // (batch, step, dim) order
+        for (int64_t j = 0; j < n; ++j) {
+            const double v = static_cast<double>(blk[at[i] + j]);
+            put(&v, 8);
+        }
+    }
+}
+
+std::string Engine::probe_csv(double dt) const {
+    if (last_run_steps_ <= 0) throw RunError("no probe traces: run() has not been called");
+    std::string s = "step,time,batch,probe_key,dim_index,value\n";
+    const std::vector<int> order = export_order(pm_);
+    if (order.empty()) return s;
+    std::vector<int64_t> at(pm_.model.probes.size());
+    int64_t o = 0;
+    for (size_t i = 0; i < at.size(); ++i) {
+        at[i] = o;
+        o += int64_t{1} * batch_ * last_run_steps_ * probe_dim(static_cast<int>(i));
+    }
+    const float* blk = probe_stage_.as<float>();
+    const int S = last_run_steps_;
+    // rows by step, batch, key, dim; steps formatted in parallel blocks
+    const int nt = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+    std::vector<std::string> part(nt);
+    auto work = [&](int t) {
+        std::string& r = part[t];
+        char buf[64];
+        for (int st = S * t / nt; st < S * (t + 1) / nt; ++st) {
+            std::snprintf(buf, sizeof buf, "%.9g", (st + 1) * dt);
+            const std::string stamp = std::to_string(st) + ',' + buf + ',';
+            for (int b = 0; b < batch_; ++b)
+                for (int i : order) {
+                    const int D = probe_dim(i);
+                    for (int d = 0; d < D; ++d) {
+                        std::snprintf(buf, sizeof buf, "%.17g",
+                                      static_cast<double>(blk[at[i] + (int64_t{1} * b * S + st) * D + d]));
+                        r += stamp;
+                        r += std::to_string(b);
+                        r += ',';
+                        r += std::to_string(pm_.model.probes[i].key);
+                        r += ',';
+                        r += std::to_string(d);
+                        r += ',';
+                        r += buf;
+                        r += '\n';
+                    }
+                }
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+    for (auto& r : part) s += r;
+    return s;
 }
 
 void Engine::device_call_args(int n_steps, const float* const* d_feeds, float* const* d_probes, const float** base_out,

@@ -75,6 +75,10 @@ class Engine {
     int shard_count() const { return shard_count_; }
     void reset();
     std::vector<double> read_signal(int sig, int batch_index) const;
+    // probe export of the last run() (export.hpp:17-30): NENG1 bytes / CSV text
+    int64_t probe_dump_bytes() const;
+    void probe_dump(char* out, int64_t capacity) const;
+    std::string probe_csv(double dt) const;
     int buffer_storage(int buffer) const;
     void synchronize();
 
@@ -134,6 +138,7 @@ class Engine {
     cudaStream_t call_stream_ = nullptr;
     cudaStream_t stream_ = nullptr;
     int64_t last_launches_ = 0;
+    int last_run_steps_ = 0;  // steps of the last run() whose probes sit in probe_stage_ ([probe][B][step][dim] f32)
 
     std::vector<BufLayout> bufs_;
     DevMem arena_, pristine_, reset_meta_;

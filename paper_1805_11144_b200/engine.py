@@ -49,6 +49,10 @@ def lib():
         L.neng_gpu_read_signal.argtypes = [P, C.c_int32, C.c_int32, C.POINTER(C.c_double), C.c_int64,
                                            C.POINTER(C.c_int64)]
         L.neng_gpu_buffer_storage.argtypes = [P, C.c_int32, C.POINTER(C.c_int32)]
+        L.neng_gpu_probe_dump_size.argtypes = [P, C.POINTER(C.c_int64)]
+        L.neng_gpu_probe_dump.argtypes = [P, C.c_void_p, C.c_int64]
+        L.neng_gpu_write_probe_binary.argtypes = [P, C.c_char_p]
+        L.neng_gpu_write_probe_csv.argtypes = [P, C.c_char_p, C.c_double]
         for fn in ("neng_gpu_batch", "neng_gpu_unroll", "neng_gpu_steps_completed", "neng_gpu_num_probes",
                    "neng_gpu_mode"):
             getattr(L, fn).argtypes = [P]
@@ -155,6 +159,21 @@ class GpuEngine:
         self._check(lib().neng_gpu_read_signal(self._h, sig, batch_index, out.ctypes.data_as(_abi.f64p), n.value,
                                                C.byref(n)))
         return out[:n.value]
+
+    # -- probe export (export.hpp:17-25) of the last run ----------------------
+    def probe_dump(self) -> bytes:
+        """NENG1 bytes of the last run's traces (write_probe_binary)."""
+        n = C.c_int64()
+        self._check(lib().neng_gpu_probe_dump_size(self._h, C.byref(n)))
+        buf = C.create_string_buffer(max(n.value, 1))
+        self._check(lib().neng_gpu_probe_dump(self._h, buf, n.value))
+        return buf.raw[:n.value]
+
+    def write_probe_binary(self, path: str):
+        self._check(lib().neng_gpu_write_probe_binary(self._h, os.fsencode(path)))
+
+    def write_probe_csv(self, path: str, dt: float):
+        self._check(lib().neng_gpu_write_probe_csv(self._h, os.fsencode(path), float(dt)))
 
     def buffer_storage(self, buffer: int) -> ir.StorageMode:
         mode = C.c_int32()
