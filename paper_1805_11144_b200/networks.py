@@ -292,6 +292,61 @@ def random_network(seed: int, n_ens: int, n: int, d: int, k_out: int, n_inputs: 
     return Workload(name, nb.m, batch, steps, feeds, n_ens * n)
 
 
+def config1(seed: int = 1, steps: int = 1000, batch: int = 64, dims: int = 64) -> Workload:
+    """Circular convolution of two `dims`-D inputs (BASELINE config 1): per batch row
+    seeded unit-norm Gaussian vectors A, B, constant over the run.  The real DFT
+    (frequencies 0..dims/2) projects A and B into 4*(dims/2+1) two-D product
+    ensembles (100 LIF each; inputs [row_a.A, row_b.B] for the re*re, im*im,
+    re*im, im*re products of each frequency); the product decoders are seeded
+    N(0, 1/100) (BASELINE leaves them unspecified; no least-squares solve); the
+    inverse real DFT maps the products onto `dims` one-D output ensembles (50
+    LIF each) as scalar-transform decoded connections.  Every synapse is a
+    lowpass with tau = 0.005 s.  Probes: the first four output ensembles'
+    decoded values."""
+    nb = NetBuilder(seed)
+    rng = np.random.default_rng(derive_seed(seed, 11) % (2 ** 63))
+    d = dims
+    nf = d // 2 + 1
+    n_idx = np.arange(d)
+    cos = np.array([np.cos(2 * np.pi * k * n_idx / d) for k in range(nf)])   # [nf][d]
+    sin = np.array([-np.sin(2 * np.pi * k * n_idx / d) for k in range(nf)])
+    node_a, a = nb.feedable_node(d, np.zeros(d))
+    node_b, b = nb.feedable_node(d, np.zeros(d))
+    prods = []  # (ensemble, frequency, type)
+    for k in range(nf):
+        for typ, (ra, rb) in enumerate(((cos, cos), (sin, sin), (cos, sin), (sin, cos))):
+            e = nb.ensemble(100, 2)
+            # (the sine rows of frequencies 0 and d/2 vanish: no connection is built for them)
+            if np.any(ra[k] != 0.0):
+                nb.connect(a, e.in_, np.vstack([ra[k], np.zeros(d)]), synapse=0.005)
+            if np.any(rb[k] != 0.0):
+                nb.connect(b, e.in_, np.vstack([np.zeros(d), rb[k]]), synapse=0.005)
+            nb.decoded(e, rng.normal(0.0, math.sqrt(1.0 / 100), size=(1, 100)))
+            prods.append((e, k, typ))
+    outs = []
+    for j in range(d):
+        e = nb.ensemble(50, 1)
+        nb.decoded(e, rng.normal(0.0, math.sqrt(1.0 / 50), size=(1, 50)))
+        outs.append(e)
+    # inverse real DFT: c_j = sum_k w_k/d (Re C_k cos - Im C_k sin), Re C = rr - ii, Im C = ri + ir
+    for (e, k, typ) in prods:
+        wk = (1.0 if k == 0 or (d % 2 == 0 and k == d // 2) else 2.0) / d
+        for j, o in enumerate(outs):
+            c, s_ = math.cos(2 * math.pi * k * j / d), math.sin(2 * math.pi * k * j / d)
+            t = wk * (c if typ == 0 else -c if typ == 1 else -s_)
+            if t != 0.0:
+                nb.connect(e.xhat, o.in_, np.array([[t]]), synapse=0.005)
+    for j in range(min(4, d)):
+        nb.probe(outs[j].xhat, f"c{j}")
+    rngf = np.random.default_rng(seed + 1000)
+    feeds = {}
+    for node in (node_a, node_b):
+        v = rngf.standard_normal((batch, d))
+        v /= np.linalg.norm(v, axis=1, keepdims=True)
+        feeds[node] = np.repeat(v[:, None, :], steps, axis=1)
+    return Workload("config1_cconv", nb.m, batch, steps, feeds, len(prods) * 100 + d * 50)
+
+
 def config2(seed: int = 1, steps: int = 1000, batch: int = 32) -> Workload:
     return random_network(seed, 256, 1024, 16, 4, 32, batch, steps, name="config2_random_256x1024")
 

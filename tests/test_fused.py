@@ -243,3 +243,18 @@ def test_captures_and_orphans_both_schedules(dataflow, monkeypatch):
         for i, (n, f) in enumerate(calls):
             assert_bitexact(gpu.run(n, f), ref.run(n, f), f"dataflow={dataflow} spl={spl} call {i}")
             full_state_equal(gpu, ref, pm.model, w.batch, f"dataflow={dataflow} spl={spl} call {i}")
+
+
+@pytest.mark.parametrize("mode", [MODE_FUSED, MODE_GENERIC])
+def test_config1_cconv_geometry_bit_exact(mode):
+    # config 1's circular-convolution structure at 16 dims (the full 64-dim graph's
+    # 132-way input fan-in makes the planner the bottleneck, not the engine):
+    # 36 two-D product ensembles fed by DFT projections, 16 one-D output ensembles
+    # fed through the inverse DFT, constant inputs, batch 4
+    w = networks.config1(steps=40, batch=4, dims=16)
+    pm = passes.run_passes(w.model)
+    gpu = GpuEngine(pm, w.batch, mode=mode)
+    assert gpu.mode() == mode
+    ref = refapi.RefEngine(pm, w.batch)
+    assert_bitexact(gpu.run(w.steps, w.feeds), ref.run(w.steps, w.feeds), "config1")
+    full_state_equal(gpu, ref, pm.model, w.batch, "config1")
