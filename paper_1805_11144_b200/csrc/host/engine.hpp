@@ -86,6 +86,7 @@ class Engine {
     int unroll() const { return unroll_; }
     int steps_completed() const { return steps_done_; }
     int mode() const { return mode_; }
+    int requested_mode() const { return requested_mode_; }
     int64_t last_launches() const { return last_launches_; }
     const PlannedModel& planned() const { return pm_; }
     int num_probes() const { return static_cast<int>(pm_.model.probes.size()); }

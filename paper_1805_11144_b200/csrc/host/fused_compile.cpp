@@ -38,6 +38,9 @@ namespace nengb {
 int fused_dmax_for(int d);
 size_t fused_smem_bytes(const FusedProgram& p, int dmax);
 cudaError_t launch_fused(const FusedProgram& p, int dmax, int grid, int k0, int k1, cudaStream_t stream);
+cudaError_t launch_feed_projection(const FProj* proj, int nproj, const float* weights, const float* feed_data,
+                                   const int64_t* feed_off, const int32_t* present, const float* arena, float* out,
+                                   int n_steps, int k0, int k1, int B, cudaStream_t stream);
 int fused_max_grid(const FusedProgram& p, int dmax, int device);
 
 namespace {
@@ -56,7 +59,9 @@ class FusedImpl : public FusedPlan {
   public:
     FusedProgram prog;
     int dmax = 8, grid = 1, steps_per_launch = 0;
-    DevMem d_ens, d_conns, d_incoming, d_orphans, d_my_conns, d_values, d_probes, d_feeds, d_call, d_prof, d_work, d_xbuf, d_df;
+    DevMem d_ens, d_conns, d_incoming, d_orphans, d_my_conns, d_values, d_probes, d_feeds, d_call, d_prof, d_work, d_xbuf, d_df, d_proj, d_projw, d_projout;
+    int n_proj = 0, proj_rows = 0;  // fed-node projections (FProj)
+    std::vector<FProj> h_proj;
     std::string desc;
 
     FusedProgram call;  // the open call's program (begin .. step)
@@ -64,16 +69,29 @@ class FusedImpl : public FusedPlan {
     void begin(int n_steps, const float* d_feed_data, const int64_t* feed_off, const int* present, float* d_ring,
                const int64_t* ring_off, cudaStream_t stream) override {
         // per-call tables: feed offsets, presence, ring offsets
-        const int nf = prog.n_feeds, np = n_probe_total;
+        cuda_check(cudaStreamSynchronize(stream), "fused call tables");  // the previous call's tables are free
+        // feed slots, then one slot per fed-node projection (computed per launch)
+        const int nf0 = prog.n_feeds, nf = nf0 + n_proj, np = n_probe_total;
+        const float* base = d_feed_data;
+        if (n_proj) {
+            d_projout.ensure(static_cast<size_t>(std::max(n_steps, 1)) * proj_rows * prog.batch * sizeof(float));
+            if (!base) base = d_projout.as<float>();
+        }
+        std::vector<int64_t> offs(feed_off, feed_off + nf0);
+        std::vector<int32_t> pres(present, present + nf0);
+        for (int q = 0; q < n_proj; ++q) {
+            offs.push_back((d_projout.as<float>() - base) + static_cast<int64_t>(h_proj[q].dd_prefix) * n_steps * prog.batch);
+            pres.push_back(1);
+        }
         std::vector<char> blob(static_cast<size_t>(nf) * 8 + static_cast<size_t>(np) * 8 + static_cast<size_t>(nf) * 4 + 64);
-        std::memcpy(blob.data(), feed_off, nf * 8);
+        std::memcpy(blob.data(), offs.data(), nf * 8);
         std::memcpy(blob.data() + nf * 8, ring_off, np * 8);
-        std::memcpy(blob.data() + nf * 8 + np * 8, present, nf * 4);
+        std::memcpy(blob.data() + nf * 8 + np * 8, pres.data(), nf * 4);
         cuda_check(cudaStreamSynchronize(stream), "fused call tables");  // the previous call's tables are free
         d_call.ensure(blob.size());
         cuda_check(cudaMemcpyAsync(d_call.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, stream), "fused call H2D");
         FusedProgram p = prog;
-        p.feed_data = d_feed_data;
+        p.feed_data = base;
         p.feed_off = d_call.as<int64_t>();
         p.ring_off = reinterpret_cast<const int64_t*>(d_call.as<char>() + nf * 8);
         p.feed_present = reinterpret_cast<const int32_t*>(d_call.as<char>() + nf * 8 + np * 8);
@@ -101,7 +119,17 @@ class FusedImpl : public FusedPlan {
         p.first_update = (flags & NENG_STEP_FIRST_UPDATE) ? 1 : 0;
         p.epilogue = (flags & NENG_STEP_EPILOGUE) ? 1 : 0;
         cuda_check(cudaMemsetAsync(d_work.p, 0, 8, stream), "fused work reset");
+        project(p, k0, k1, stream);
         cuda_check(launch_fused(p, dmax, grid, k0, k1, stream), "fused kernel launch");
+    }
+
+    /// the fed-node projections of steps [k0, k1) (before the launch that reads them)
+    void project(const FusedProgram& p, int k0, int k1, cudaStream_t stream) {
+        if (!n_proj) return;
+        cuda_check(launch_feed_projection(d_proj.as<FProj>(), n_proj, d_projw.as<float>(), p.feed_data, p.feed_off,
+                                          p.feed_present, p.arena, d_projout.as<float>(), p.call_steps, k0, k1,
+                                          p.batch, stream),
+                   "feed projection");
     }
 
     void xhat_layout(int64_t* xbuf_floats, int64_t* rank_floats, float** xbuf) const override {
@@ -133,6 +161,7 @@ class FusedImpl : public FusedPlan {
             p.dataflow = dataflow ? 1 : 0;
             cuda_check(cudaMemsetAsync(d_work.p, 0, dataflow ? 16 + static_cast<size_t>(units) * 4 : 8, stream),
                        "fused work reset");
+            project(p, k, std::min(n_steps, k + K), stream);
             cuda_check(launch_fused(p, dmax, grid, k, std::min(n_steps, k + K), stream), "fused kernel launch");
             ++launches;
         }
@@ -333,6 +362,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             int dot, rst, sp, copy;
             int src, T, accs, filt, state;
             int dst_ens;
+            bool proj;  // fed node wider than the fused rows: projected ahead of the kernel (FProj)
         };
         std::vector<ConnInfo> conns;
         std::unordered_map<int, int> conn_of_copy, conn_of_filt, conn_of_state;
@@ -389,7 +419,13 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             const Signal& Ts = m.signals[c.T];
             int dd = m.signals[c.accs].rows(), ds = m.signals[c.src].rows();
             if (Ts.shape.size() != 2 || Ts.shape[0] != dd || Ts.shape[1] != ds) fail("transform shape");
-            if (!fused_dmax_for(std::max(dd, ds))) fail("dimension above 32");
+            c.proj = false;
+            if (!fused_dmax_for(std::max(dd, ds))) {
+                if (slot_of_sig.count(c.src) && fused_dmax_for(dd))
+                    c.proj = true;
+                else
+                    fail("dimension above 32");
+            }
             for (int o : {c.dot, c.rst, c.sp}) claim(o);
             if (c.copy >= 0) {
                 claim(c.copy);
@@ -431,7 +467,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         for (const EnsInfo& e : ens)
             dmax_need = std::max({dmax_need, m.signals[e.in].rows(), m.signals[e.xhat].rows()});
         for (const ConnInfo& c : conns)
-            dmax_need = std::max({dmax_need, m.signals[c.accs].rows(), m.signals[c.src].rows()});
+            dmax_need = std::max({dmax_need, m.signals[c.accs].rows(), c.proj ? 0 : m.signals[c.src].rows()});
         const int DMAX = fused_dmax_for(dmax_need);
         auto align4 = [&] {
             while (values.size() % 4) values.push_back(0.0f);
@@ -523,7 +559,19 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             fe.push_back(x);
         }
         xrows = W * xstride;
+        {
+            // a unit applies its incoming connections one after another (a chain of
+            // dependent loads); past this fan-in the generic executor is faster
+            // (config 1's 132-way inverse DFT: 2.6 vs 0.6 ms/step), so AUTO keeps it
+            int fan_in = 0;
+            for (const FEns& x : fe) fan_in = std::max(fan_in, x.inc_count);
+            if (fan_in > 64 && eng.requested_mode() == NENG_MODE_AUTO && W == 1)
+                fail("fan-in " + std::to_string(fan_in) + " above 64 (the generic executor is faster)");
+        }
         std::vector<FConn> fc;
+        std::vector<FProj> projs;
+        std::vector<float> proj_w;
+        int proj_rows = 0;
         for (const ConnInfo& c : conns) {
             FConn x{};
             x.src_base = eng.resolve_full(c.src).base;
@@ -542,7 +590,28 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
                 if (m.feed_slots[x.src_feed].dim != x.ds) fail("feed slot dim differs from its signal");
             }
             x.acc_init_off = push_values(m.operators[c.rst].value);
-            {
+            if (c.proj) {
+                // T . u computed ahead of the kernel into projection slot n_feeds + q; the
+                // connection reads it through an identity transform (see FProj)
+                const Signal& Ts = m.signals[c.T];
+                FProj pj{};
+                pj.t_off = static_cast<int64_t>(proj_w.size());
+                for (size_t i = 0; i < static_cast<size_t>(x.dd) * x.ds; ++i)
+                    proj_w.push_back(Ts.initial.empty() ? 0.0f : static_cast<float>(Ts.initial[i]));
+                pj.node_base = x.src_base;
+                pj.slot = x.src_feed;
+                pj.dd = x.dd;
+                pj.ds = x.ds;
+                pj.copies = per_batch(c.src) ? B : 1;
+                pj.dd_prefix = proj_rows;
+                proj_rows += x.dd;
+                x.src_feed = static_cast<int32_t>(m.feed_slots.size() + projs.size());
+                projs.push_back(pj);
+                x.ds = x.dd;
+                x.tpad_off = align4();
+                for (int rr = 0; rr < x.dd; ++rr)
+                    for (int jj = 0; jj < DMAX; ++jj) values.push_back(jj == rr ? 1.0f : 0.0f);
+            } else {
                 const Signal& Ts = m.signals[c.T];
                 x.tpad_off = align4();
                 for (int rr = 0; rr < x.dd; ++rr)
@@ -668,6 +737,11 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         upload(impl->d_values, values.data(), values.size() * sizeof(float));
         upload(impl->d_probes, fp.data(), fp.size() * sizeof(FProbe));
         upload(impl->d_feeds, ff.data(), ff.size() * sizeof(FFeed));
+        upload(impl->d_proj, projs.data(), projs.size() * sizeof(FProj));
+        upload(impl->d_projw, proj_w.data(), proj_w.size() * sizeof(float));
+        impl->n_proj = static_cast<int>(projs.size());
+        impl->h_proj = projs;
+        impl->proj_rows = proj_rows;
         p.arena = eng.arena();
         p.values = impl->d_values.as<float>();
         p.ens = impl->d_ens.as<FEns>();

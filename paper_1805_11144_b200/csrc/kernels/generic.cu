@@ -367,6 +367,45 @@ cudaError_t launch_feed_transpose(const float* in, float* out, const int64_t* of
     return cudaGetLastError();
 }
 
+/// Fed-node projections (FProj) for steps [k0, k1) of an n_steps call: projection q
+/// is the block [n_steps][dd][B] at out + dd_prefix * n_steps * B (a feed-slot layout).
+__global__ void feed_projection_kernel(const FProj* proj, int nproj, const float* weights, const float* feed_data,
+                                       const int64_t* feed_off, const int32_t* present, const float* arena,
+                                       float* out, int n_steps, int k0, int k1, int B) {
+    const int q = blockIdx.y;
+    if (q >= nproj) return;
+    const FProj P = proj[q];
+    const int64_t n = static_cast<int64_t>(k1 - k0) * P.dd * B;
+    const bool fed = present[P.slot] != 0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int b = static_cast<int>(i % B);
+        const int64_t kr = i / B;
+        const int r = static_cast<int>(kr % P.dd);
+        const int k = k0 + static_cast<int>(kr / P.dd);
+        const float* T = weights + P.t_off + static_cast<int64_t>(r) * P.ds;
+        float acc = 0.0f;
+        if (fed) {
+            const float* u = feed_data + feed_off[P.slot] + static_cast<int64_t>(k) * P.ds * B + b;
+            for (int j = 0; j < P.ds; ++j) acc = acc + T[j] * u[static_cast<int64_t>(j) * B];
+        } else {
+            const float* u = arena + P.node_base + (P.copies > 1 ? b : 0);
+            for (int j = 0; j < P.ds; ++j) acc = acc + T[j] * u[static_cast<int64_t>(j) * P.copies];
+        }
+        out[static_cast<int64_t>(P.dd_prefix) * n_steps * B + (static_cast<int64_t>(k) * P.dd + r) * B + b] = acc;
+    }
+}
+
+cudaError_t launch_feed_projection(const FProj* proj, int nproj, const float* weights, const float* feed_data,
+                                   const int64_t* feed_off, const int32_t* present, const float* arena, float* out,
+                                   int n_steps, int k0, int k1, int B, cudaStream_t stream) {
+    if (nproj == 0 || k1 <= k0) return cudaSuccess;
+    dim3 grid(64, nproj);
+    feed_projection_kernel<<<grid, 256, 0, stream>>>(proj, nproj, weights, feed_data, feed_off, present, arena, out,
+                                                     n_steps, k0, k1, B);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_reset(float* arena, const float* pristine, const int64_t* base, const int64_t* pbase,
                          const int64_t* span, const int32_t* per_batch, int nbuf, int B, cudaStream_t stream) {
     if (nbuf == 0) return cudaSuccess;

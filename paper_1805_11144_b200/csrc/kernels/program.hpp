@@ -16,6 +16,21 @@
 
 namespace nengb {
 
+/// A fed-node connection wider than the fused pipeline's rows (ds > 32): its
+/// DotInc sum y = +0 + sum_j T[r,j]*u[j] (j ascending, rounded products and
+/// sums) is computed ahead of the fused kernel for the launch's steps, and the
+/// connection then reads y through an identity transform (exact: a running sum
+/// from +0 is never -0, so adding the zero terms leaves y unchanged).
+struct FProj {
+    int64_t t_off;      // T [dd][ds] f32 in the projection weights
+    int64_t node_base;  // arena base of the fed node's signal (read when its feed is absent)
+    int32_t slot;       // the fed node's feed slot
+    int32_t dd, ds;
+    int32_t copies;     // B when the node is per-batch, else 1
+    int32_t dd_prefix;  // sum of dd over the earlier projections: output rows [dd_prefix, +dd) of [step][rows][B]
+    int32_t pad_;
+};
+
 struct DArg {
     int64_t base = 0;  // arena offset (floats) of element 0
     int64_t elems = 0; // rows * elements-per-row of the operand

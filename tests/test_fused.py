@@ -258,3 +258,17 @@ def test_config1_cconv_geometry_bit_exact(mode):
     ref = refapi.RefEngine(pm, w.batch)
     assert_bitexact(gpu.run(w.steps, w.feeds), ref.run(w.steps, w.feeds), "config1")
     full_state_equal(gpu, ref, pm.model, w.batch, "config1")
+
+
+def test_wide_fed_connections_projected_ahead_of_the_kernel():
+    # 40-D inputs: the DFT projections (2 x 40 transforms from fed nodes) exceed the fused
+    # rows, so they are computed ahead of each launch and read through an identity
+    # transform; a second call without feeds takes the nodes' default values from the arena
+    w = networks.config1(steps=25, batch=3, dims=40)
+    pm = passes.run_passes(w.model)
+    gpu = GpuEngine(pm, w.batch, mode=MODE_FUSED)
+    ref = refapi.RefEngine(pm, w.batch)
+    assert_bitexact(gpu.run(w.steps, w.feeds), ref.run(w.steps, w.feeds), "projected feeds")
+    full_state_equal(gpu, ref, pm.model, w.batch, "projected feeds")
+    assert_bitexact(gpu.run(7), ref.run(7), "default node values")
+    full_state_equal(gpu, ref, pm.model, w.batch, "default node values")
