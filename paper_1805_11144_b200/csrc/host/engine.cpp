@@ -542,6 +542,26 @@ void Engine::compile_generic() {
         g.n_members = static_cast<int32_t>(members.size()) - g.member_begin;
         g.n_tiles = static_cast<int32_t>(tiles.size()) - g.tile_begin;
         g.flags |= GF_BARRIER;
+        if (first.kind == OpKind::DotInc && batch_ >= 64 && (g.flags & GF_PER_BATCH) &&
+            !(g.flags & (GF_SERIAL_ALL | GF_SERIAL_B)) && std::getenv("NENG_GENERIC_DENSE_OFF") == nullptr) {
+            // dense members (shared row-major A, per-batch x and y, at least 32 x 32): CTA
+            // tiles of 32 rows x 64 batch columns (dense_dot_tile) instead of one thread per output
+            bool dense = true;
+            for (int mi = g.member_begin; mi < static_cast<int>(members.size()) && dense; ++mi) {
+                const DArg &A = members[mi].a[0], &X = members[mi].a[1], &Y = members[mi].a[2];
+                dense = A.bs == 0 && A.es == 1 && A.elems == Y.elems * X.elems && X.es == batch_ && X.bs == 1 &&
+                        Y.es == batch_ && Y.bs == 1 && Y.elems >= 32 && X.elems >= 32;
+            }
+            if (dense) {
+                tiles.resize(g.tile_begin);
+                for (int mi = g.member_begin; mi < static_cast<int>(members.size()); ++mi)
+                    for (int64_t r0 = 0; r0 < members[mi].a[2].elems; r0 += 32)
+                        for (int c0 = 0; c0 < batch_; c0 += 64)
+                            tiles.push_back({mi, static_cast<int32_t>(r0), c0});
+                g.n_tiles = static_cast<int32_t>(tiles.size()) - g.tile_begin;
+                g.flags |= GF_DENSE;
+            }
+        }
         if (precision_ == NENG_PRECISION_TF32 && first.kind == OpKind::DotInc && batch_ >= 32 &&
             (g.flags & GF_PER_BATCH) && !(g.flags & (GF_SERIAL_ALL | GF_SERIAL_B))) {
             // C[M][B] += A[M][K] X[K][B]: shared row-major weights, per-batch input and output

@@ -118,6 +118,69 @@ __device__ __forceinline__ void exec_item(const GenericProgram& p, const DGroup&
     }
 }
 
+// DotInc on a 32-row x 64-column (batch) output tile of one member, by the
+// whole CTA: A [M][K] shared row-major, x [K][B] and y [M][B] per-batch.  Each
+// output keeps the reference's sum (acc = +0; acc += A[r,k]*x[k] for k
+// ascending, each product and sum rounded; y += acc); A and x are staged
+// through shared memory 32 k at a time.  Padding rows/columns hold +0, and a
+// running sum from +0 is never -0, so the zero terms change nothing.
+constexpr int kDTM = 32, kDTN = 64, kDTK = 32;  // 2 rows x 4 columns per thread
+__device__ void dense_dot_tile(const GenericProgram& p, const DMember& m, int row0, int col0) {
+    __shared__ float As[kDTK][kDTM + 4];
+    __shared__ __align__(16) float Xs[kDTK][kDTN];
+    const int B = p.batch;
+    const int64_t M = m.a[2].elems, K = m.a[1].elems;
+    const float* A = p.arena + m.a[0].base;
+    const float* X = p.arena + m.a[1].base;
+    float* Y = p.arena + m.a[2].base;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    float acc[2][4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+    for (int64_t k0 = 0; k0 < K; k0 += kDTK) {
+#pragma unroll
+        for (int i = 0; i < (kDTM * kDTK) / 256; ++i) {
+            const int idx = threadIdx.x + i * 256;
+            const int r = idx / kDTK, kk = idx - r * kDTK;
+            const int64_t gr = row0 + r, gk = k0 + kk;
+            As[kk][r] = (gr < M && gk < K) ? A[gr * K + gk] : 0.0f;
+        }
+#pragma unroll
+        for (int i = 0; i < (kDTN * kDTK) / 256; ++i) {
+            const int idx = threadIdx.x + i * 256;
+            const int kk = idx / kDTN, c = idx - kk * kDTN;
+            const int64_t gk = k0 + kk;
+            const int gc = col0 + c;
+            Xs[kk][c] = (gk < K && gc < B) ? X[gk * B + gc] : 0.0f;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < kDTK; ++kk) {
+            const float4 xv = *reinterpret_cast<const float4*>(&Xs[kk][tx * 4]);
+            const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const float a = As[kk][ty * 2 + i];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = acc[i][j] + a * xs[j];
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int64_t r = row0 + ty * 2 + i;
+        if (r >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int c = col0 + tx * 4 + j;
+            if (c < B) Y[r * B + c] = Y[r * B + c] + acc[i][j];
+        }
+    }
+}
+
 // Reference loop order for one member and one copy b (GF_SERIAL_ALL).
 __device__ void exec_member_serial(const GenericProgram& p, const DGroup& g, const DMember& m, int b) {
     switch (g.kind) {
@@ -223,6 +286,11 @@ __global__ void __launch_bounds__(kTile) generic_run_kernel(GenericProgram p, in
                         }
                         __syncthreads();
                     }
+            } else if (g.flags & GF_DENSE) {
+                for (int t = blockIdx.x; t < g.n_tiles; t += gridDim.x) {
+                    const DTile tl = p.tiles[g.tile_begin + t];
+                    dense_dot_tile(p, p.members[tl.member], tl.start, tl.count);
+                }
             } else {
                 for (int t = blockIdx.x; t < g.n_tiles; t += gridDim.x) {
                     const DTile tl = p.tiles[g.tile_begin + t];

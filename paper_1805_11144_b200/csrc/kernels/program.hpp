@@ -45,6 +45,7 @@ enum : int32_t {
     GF_SERIAL_ALL = 8,  // a member aliases itself with an offset: reference loop order, one thread
     GF_HAS_STATE = 16,  // SimProcess with a state operand (tau > 0)
     GF_BARRIER = 32,    // grid barrier after this group
+    GF_DENSE = 64,      // DotInc with shared row-major A, per-batch x and y: CTA tiles (DTile = member, row0, col0)
 };
 
 enum : int32_t { MF_SCALAR_A = 1 };

@@ -267,3 +267,19 @@ def test_config3_strict_matches_reference_and_tf32_within_tolerance():
     assert np.abs(a).max() > 0.1  # the network is active
     rel = np.linalg.norm(a - b) / np.linalg.norm(a)
     assert rel < 0.10, rel
+
+
+def test_dense_dot_tiles_bit_exact():
+    # batch >= 64: the interpreter runs config 3's dense layers (shared 1024 x 784 and
+    # 1024 x 1024 weights) as CTA tiles of 32 rows x 64 batch columns staged through
+    # shared memory, keeping each output's sequential sum; batch 80 leaves a partial
+    # column tile, 1024 rows are whole row tiles, the 10-row output layer stays per-thread
+    w = networks.config3(steps=6, batch=80)
+    pm = passes.run_passes(w.model)
+    ref = refapi.RefEngine(pm, w.batch)
+    gpu = GpuEngine(pm, w.batch, mode=MODE_GENERIC)
+    assert_bitexact(gpu.run(w.steps, w.feeds), ref.run(w.steps, w.feeds), "dense tiles")
+    for s in pm.model.signals:
+        if s.label.endswith(".J") or s.label.endswith("accum"):
+            for b in (0, w.batch - 1):
+                assert np.array_equal(gpu.read_signal(s.id, b).view(np.uint64), ref.read_signal(s.id, b).view(np.uint64)), s.label
