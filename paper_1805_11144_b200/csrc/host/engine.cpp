@@ -544,13 +544,13 @@ void Engine::compile_generic() {
         g.flags |= GF_BARRIER;
         if (first.kind == OpKind::DotInc && batch_ >= 64 && (g.flags & GF_PER_BATCH) &&
             !(g.flags & (GF_SERIAL_ALL | GF_SERIAL_B)) && std::getenv("NENG_GENERIC_DENSE_OFF") == nullptr) {
-            // dense members (shared row-major A, per-batch x and y, at least 32 x 32): CTA
+            // dense members (shared row-major A, per-batch x and y, K >= 32): CTA
             // tiles of 32 rows x 64 batch columns (dense_dot_tile) instead of one thread per output
             bool dense = true;
             for (int mi = g.member_begin; mi < static_cast<int>(members.size()) && dense; ++mi) {
                 const DArg &A = members[mi].a[0], &X = members[mi].a[1], &Y = members[mi].a[2];
                 dense = A.bs == 0 && A.es == 1 && A.elems == Y.elems * X.elems && X.es == batch_ && X.bs == 1 &&
-                        Y.es == batch_ && Y.bs == 1 && Y.elems >= 32 && X.elems >= 32;
+                        Y.es == batch_ && Y.bs == 1 && X.elems >= 32;  // any rows: a long k loop per thread is latency-bound
             }
             if (dense) {
                 tiles.resize(g.tile_begin);

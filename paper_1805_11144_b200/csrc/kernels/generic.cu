@@ -63,6 +63,7 @@ __device__ __forceinline__ void exec_item(const GenericProgram& p, const DGroup&
             const float* x = at(p, m.a[1], 0, b);
             const int32_t xes = m.a[1].es;
             float acc = 0.0f;
+#pragma unroll 8
             for (int64_t k = 0; k < n; ++k) acc = acc + arow[k * aes] * x[k * xes];
             float* y = at(p, m.a[2], local, b);
             *y = *y + acc;
