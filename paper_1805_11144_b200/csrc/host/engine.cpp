@@ -573,7 +573,7 @@ void Engine::compile_generic() {
                 const DArg &A = dm.a[0], &X = dm.a[1], &Y = dm.a[2];
                 const int64_t M = Y.elems, K = X.elems;
                 ok = A.bs == 0 && A.es == 1 && A.elems == M * K && X.es == batch_ && X.bs == 1 && Y.es == batch_ &&
-                     Y.bs == 1 && M >= 32 && K >= 32;
+                     Y.bs == 1 && M >= 1 && K >= 32;
                 if (ok) tg.gemms.push_back({A.base, X.base, Y.base, static_cast<int>(M), static_cast<int>(K)});
             }
             if (ok) tc_groups_.push_back(std::move(tg));
