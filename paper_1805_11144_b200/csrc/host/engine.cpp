@@ -534,8 +534,14 @@ void Engine::compile_generic() {
                 }
             int64_t total_items = dm.items * g.copies;
             int mi = static_cast<int>(members.size());
-            for (int64_t s = 0; s < total_items; s += kTile)
-                tiles.push_back({mi, static_cast<int32_t>(s), static_cast<int32_t>(std::min<int64_t>(kTile, total_items - s))});
+            // light items (Reset, Copy, ElementwiseInc, SimProcess) of large members: 4 per
+            // thread per tile (amortises the descriptor loads); heavy ones (a DotInc k loop,
+            // a neuron step) and small members: 1 per thread, for load balance and latency
+            const bool heavy = op.kind == OpKind::DotInc || op.kind == OpKind::SimNeurons || op.kind == OpKind::SimPES;
+            const int64_t per_tile = heavy || total_items < (int64_t{1} << 18) ? kTile : kTileItems;
+            for (int64_t s = 0; s < total_items; s += per_tile)
+                tiles.push_back(
+                    {mi, static_cast<int32_t>(s), static_cast<int32_t>(std::min<int64_t>(per_tile, total_items - s))});
             if (total_items > (int64_t{1} << 30)) throw BuildError("group member too large for the generic path");
             members.push_back(dm);
         }
@@ -625,6 +631,14 @@ void Engine::compile_generic() {
     if (needs_libm_) prog_.libm = libm_tables(device_);
 
     int maxco = generic_max_coresident_blocks(device_);
+    {
+        // at most 2 CTAs per SM: every group ends in a grid barrier, whose cost grows with
+        // the CTA count (config 3 strict: 0.30 ms/step at 2 per SM, 0.35 at 3)
+        int sms = 0;
+        cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_), "SM count");
+        maxco = std::min(maxco, 2 * std::max(sms, 1));
+    }
+    if (const char* env = std::getenv("NENG_GENERIC_GRID")) maxco = std::max(1, std::min(maxco, std::atoi(env)));
     grid_ = std::max(1, std::min(maxco, max_tiles));
     // tiny programs: one CTA, block-level barriers only
     if (max_tiles <= 2) grid_ = 1;

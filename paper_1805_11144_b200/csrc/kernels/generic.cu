@@ -282,8 +282,10 @@ __global__ void __launch_bounds__(kTile) generic_run_kernel(GenericProgram p, in
                         for (int t = 0; t < g.n_tiles; ++t) {
                             const DTile tl = p.tiles[g.tile_begin + t];
                             const DMember& m = p.members[tl.member];
-                            int i = tl.start + threadIdx.x;
-                            if (threadIdx.x < tl.count && i % g.copies == b) exec_item(p, g, m, i / g.copies, b);
+                            for (int j = threadIdx.x; j < tl.count; j += blockDim.x) {
+                                const int i = tl.start + j;
+                                if (i % g.copies == b) exec_item(p, g, m, i / g.copies, b);
+                            }
                         }
                         __syncthreads();
                     }
@@ -295,11 +297,11 @@ __global__ void __launch_bounds__(kTile) generic_run_kernel(GenericProgram p, in
             } else {
                 for (int t = blockIdx.x; t < g.n_tiles; t += gridDim.x) {
                     const DTile tl = p.tiles[g.tile_begin + t];
-                    if (threadIdx.x < tl.count) {
-                        const DMember& m = p.members[tl.member];
-                        int64_t i = tl.start + threadIdx.x;
-                        int64_t local = i / g.copies;
-                        exec_item(p, g, m, local, static_cast<int>(i - local * g.copies));
+                    const DMember& m = p.members[tl.member];
+                    for (int j = threadIdx.x; j < tl.count; j += blockDim.x) {
+                        const int i = tl.start + j;  // < 2^30 (engine.cpp)
+                        const int local = i / g.copies;
+                        exec_item(p, g, m, local, i - local * g.copies);
                     }
                 }
             }

@@ -66,9 +66,10 @@ struct DGroup {
     float dt = 0.f, tau_a = 0.f, tau_b = 0.f, tau_rc = 0.f, tau_ref = 0.f, amplitude = 0.f;
 };
 
-// A tile is up to kTile consecutive work items of one member; item index
+// A tile is up to kTileItems consecutive work items of one member; item index
 // i = local * copies + b (batch innermost for coalescing).
-constexpr int kTile = 256;
+constexpr int kTile = 256;        // threads per CTA of the interpreter
+constexpr int kTileItems = 1024;  // light work items per tile (4 per thread: the descriptor loads are amortised)
 struct DTile {
     int32_t member = 0, start = 0, count = 0;
 };
