@@ -462,6 +462,9 @@ void Engine::compile_generic() {
             g.tau_rc = static_cast<float>(first.neuron.tau_rc);
             g.tau_ref = static_cast<float>(first.neuron.tau_ref);
             g.amplitude = static_cast<float>(first.neuron.amplitude);
+            volatile float mdt = -g.dt, trc = g.tau_rc;  // -delta / tau_rc in float, delta = dt
+            const float arg = mdt / trc;
+            g.em_dt = expm1f(arg);  // the host libm result the reference uses
         } else if (first.kind == OpKind::SimProcess) {
             double a = 0.0, b = 1.0;  // lowpass_coefficients (neuron_math.hpp:33-37)
             if (first.tau > 0.0) {

@@ -76,7 +76,7 @@ __device__ __forceinline__ void exec_item(const GenericProgram& p, const DGroup&
                 float* vp = at(p, m.a[2], local, b);
                 float* rp = at(p, m.a[3], local, b);
                 float v = *vp, r = *rp;
-                float o = lif_spike_step(j, v, r, g.dt, g.tau_rc, g.tau_ref, g.amplitude, p.libm);
+                float o = lif_spike_step(j, v, r, g.dt, g.tau_rc, g.tau_ref, g.amplitude, p.libm, g.em_dt);
                 *out = o;  // write order of exec.cpp:252-254 (last write wins on aliasing)
                 *vp = v;
                 *rp = r;

@@ -196,11 +196,13 @@ __device__ __forceinline__ float glibc_spec_resolved(float x, bool is_log, const
 /// lif_spike_step<float> (neuron_math.hpp:55-77), operation for operation.
 /// No FMA contraction anywhere (built with -fmad=false).
 __device__ __forceinline__ float lif_spike_step(float j, float& voltage, float& refractory, float dt, float tau_rc,
-                                                float tau_ref, float amplitude, const LibmTables& t) {
+                                                float tau_ref, float amplitude, const LibmTables& t, float em_dt) {
     float delta = dt - refractory;
     if (delta < 0.0f) delta = 0.0f;
     if (delta > dt) delta = dt;
-    float v = voltage - (j - voltage) * glibc_expm1f(-delta / tau_rc, t);
+    // delta == dt (not refractory): the same argument -dt / tau_rc every step, so em_dt
+    // (the host's glibc expm1f of it) is the value expm1f returns here
+    float v = voltage - (j - voltage) * (delta == dt ? em_dt : glibc_expm1f(-delta / tau_rc, t));
     if (v < 0.0f) v = 0.0f;
     float out;
     if (v > 1.0f) {

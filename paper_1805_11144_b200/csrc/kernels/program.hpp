@@ -64,6 +64,7 @@ struct DGroup {
     int32_t tile_begin = 0, n_tiles = 0;
     int32_t copies = 1;
     float dt = 0.f, tau_a = 0.f, tau_b = 0.f, tau_rc = 0.f, tau_ref = 0.f, amplitude = 0.f;
+    float em_dt = 0.f;  // LIF: glibc expm1f(-dt / tau_rc) from the host (the step of a non-refractory neuron)
 };
 
 // A tile is up to kTileItems consecutive work items of one member; item index
