@@ -54,7 +54,8 @@ def test_fused_matches_generic_and_persists_across_calls():
 def test_config0_integrator_bit_exact():
     w = networks.config0(steps=1000)
     pm = passes.run_passes(w.model)
-    gpu = GpuEngine(pm, w.batch)
+    assert GpuEngine(pm, w.batch).mode() == MODE_GENERIC  # one unit per step: AUTO keeps the interpreter
+    gpu = GpuEngine(pm, w.batch, mode=MODE_FUSED)
     assert gpu.mode() == MODE_FUSED
     ref = refapi.RefEngine(pm, w.batch)
     assert_bitexact(gpu.run(w.steps, w.feeds), ref.run(w.steps, w.feeds), "config0")
