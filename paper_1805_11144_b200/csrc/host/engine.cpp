@@ -643,8 +643,10 @@ void Engine::compile_generic() {
     }
     if (const char* env = std::getenv("NENG_GENERIC_GRID")) maxco = std::max(1, std::min(maxco, std::atoi(env)));
     grid_ = std::max(1, std::min(maxco, max_tiles));
-    // tiny programs: one CTA, block-level barriers only
-    if (max_tiles <= 2) grid_ = 1;
+    // tiny programs: one CTA, block-level barriers only (config 0: 42 vs 60 us/step on 4 CTAs)
+    if (max_tiles <= 16 && !std::getenv("NENG_GENERIC_GRID")) grid_ = 1;
+    if (std::getenv("NENG_GENERIC_VERBOSE"))
+        std::fprintf(stderr, "[generic] %zu groups, max tiles %d, grid %d\n", groups.size(), max_tiles, grid_);
 }
 
 void Engine::reset() {

@@ -568,7 +568,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             if (fan_in > 64 && eng.requested_mode() == NENG_MODE_AUTO && W == 1)
                 fail("fan-in " + std::to_string(fan_in) + " above 64 (the generic executor is faster)");
             // a step of fewer than 4 units runs on as many CTAs: the interpreter spreads the
-            // same work over the whole GPU (config 0, one ensemble at B=1: 57 vs 113 us/step)
+            // same work over the whole GPU (config 0, one ensemble at B=1: 42 vs 113 us/step)
             const int64_t step_units = static_cast<int64_t>(fe.size()) * ((B + 255) / 256);
             if (step_units < 4 && eng.requested_mode() == NENG_MODE_AUTO && W == 1)
                 fail("only " + std::to_string(step_units) + " unit(s) per step (the generic executor is faster)");
