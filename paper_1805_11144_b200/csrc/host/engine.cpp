@@ -341,6 +341,9 @@ Engine::~Engine() {
     if (cublas_) cublasDestroy(static_cast<cublasHandle_t>(cublas_));
     for (cudaEvent_t& ev : feed_events_)
         if (ev) cudaEventDestroy(ev);
+    for (cudaEvent_t& ev : xpose_events_)
+        if (ev) cudaEventDestroy(ev);
+    if (copy_stream_) cudaStreamDestroy(copy_stream_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -831,6 +834,9 @@ void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probe
     if (!feed_events_[0]) {
         cuda_check(cudaEventCreateWithFlags(&feed_events_[0], cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&feed_events_[1], cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&xpose_events_[0], cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&xpose_events_[1], cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
     }
     double t_conv = 0.0;
     auto stage_chunk = [&](int c0, int c1, int buf) {
@@ -872,17 +878,24 @@ void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probe
         }
         t_conv += std::chrono::duration<double>(std::chrono::steady_clock::now() - tc).count();
         char* meta = feed_meta_.as<char>() + meta_stride * buf;
-        cuda_check(cudaMemcpyAsync(raw, stage, at * sizeof(float), cudaMemcpyHostToDevice, stream_), "feed H2D");
-        cuda_check(cudaMemcpyAsync(meta, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice, stream_), "feed meta");
-        cuda_check(cudaMemcpyAsync(meta + offs.size() * 8, cols.data(), cols.size() * 4, cudaMemcpyHostToDevice,
-                                   stream_),
+        // the copies run on their own stream so they overlap the previous chunk's kernel:
+        // they wait for the last transpose that read raw/meta[buf], and the transpose
+        // of this chunk waits for them
+        cuda_check(cudaStreamWaitEvent(copy_stream_, xpose_events_[buf], 0), "feed copy wait");
+        cuda_check(cudaMemcpyAsync(raw, stage, at * sizeof(float), cudaMemcpyHostToDevice, copy_stream_), "feed H2D");
+        cuda_check(cudaMemcpyAsync(meta, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice, copy_stream_),
                    "feed meta");
-        cuda_check(cudaEventRecord(feed_events_[buf], stream_), "feed event");
+        cuda_check(cudaMemcpyAsync(meta + offs.size() * 8, cols.data(), cols.size() * 4, cudaMemcpyHostToDevice,
+                                   copy_stream_),
+                   "feed meta");
+        cuda_check(cudaEventRecord(feed_events_[buf], copy_stream_), "feed event");
+        cuda_check(cudaStreamWaitEvent(stream_, feed_events_[buf], 0), "feed wait");
         const int max_cols = *std::max_element(cols.begin(), cols.end());
         cuda_check(launch_feed_transpose(raw, feed_buf_.as<float>(), reinterpret_cast<const int64_t*>(meta),
                                          reinterpret_cast<const int32_t*>(meta + offs.size() * 8),
                                          static_cast<int>(slots.size()), max_cols, B, stream_),
                    "feed transpose");
+        cuda_check(cudaEventRecord(xpose_events_[buf], stream_), "transpose event");
     };
     const bool tprof = std::getenv("NENG_RUN_PROFILE") != nullptr;  // host-side phase times (stderr)
     auto now = [] { return std::chrono::steady_clock::now(); };

@@ -158,6 +158,8 @@ class Engine {
     // per-call scratch
     DevMem feed_buf_, feed_raw_, feed_meta_, ring_, probe_out_, probe_meta_;
     cudaEvent_t feed_events_[2] = {nullptr, nullptr};  // staging-buffer reuse (pipelined host feeds)
+    cudaEvent_t xpose_events_[2] = {nullptr, nullptr};  // device raw-buffer reuse (transpose done)
+    cudaStream_t copy_stream_ = nullptr;                 // feed H2D copies overlap the kernels
     PinnedMem feed_stage_, probe_stage_;
 };
 
