@@ -252,6 +252,14 @@ int32_t neng_gpu_mode(const neng_engine* e);
 /* Kernel launches issued by the most recent run call (for the bench). */
 int64_t neng_gpu_last_launch_count(const neng_engine* e);
 
+/* Schedules the most recent run / run_device / stepped call used (bit set):
+ * the generic interpreter, the fused pipeline with one grid barrier per step,
+ * the fused pipeline's barrier-free stepping. */
+#define NENG_SCHED_GENERIC 1
+#define NENG_SCHED_FUSED_STEPPED 2
+#define NENG_SCHED_FUSED_BARRIER_FREE 4
+int32_t neng_gpu_last_schedule(const neng_engine* e);
+
 /* Error text of the engine's last failing call ("" if none). */
 const char* neng_gpu_last_error(const neng_engine* e);
 /* Error text of the calling thread's last failing call (covers create). */

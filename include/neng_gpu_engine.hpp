@@ -84,7 +84,7 @@ class GpuEngine {
             std::copy(flat.begin() + static_cast<std::ptrdiff_t>(at),
                       flat.begin() + static_cast<std::ptrdiff_t>(at + t.data.size()), t.data.begin());
             at += t.data.size();
-            out.emplace(key, std::move(t));
+            out.insert_or_assign(key, std::move(t));  // a key bound twice: the last binding wins, as capture_probes
         }
         return out;
     }

@@ -182,6 +182,7 @@ int32_t neng_gpu_steps_completed(const neng_engine* e) { return e ? e->impl.step
 int32_t neng_gpu_num_probes(const neng_engine* e) { return e ? e->impl.num_probes() : 0; }
 int32_t neng_gpu_mode(const neng_engine* e) { return e ? e->impl.mode() : 0; }
 int64_t neng_gpu_last_launch_count(const neng_engine* e) { return e ? e->impl.last_launches() : 0; }
+int32_t neng_gpu_last_schedule(const neng_engine* e) { return e ? e->impl.last_schedule() : 0; }
 
 neng_status neng_gpu_probe_info(const neng_engine* e, int32_t i, int32_t* key, int32_t* dim) {
     if (!e || i < 0 || i >= e->impl.num_probes()) return NENG_INVALID_ARGUMENT;

@@ -654,6 +654,7 @@ void Engine::compile_generic() {
 
 void Engine::reset() {
     // exec.cpp:164-174
+    if (call_steps_) throw RunError("reset: a stepped call is open");
     size_t nbuf = bufs_.size();
     const int64_t* meta = reset_meta_.as<int64_t>();
     const int32_t* pb = reinterpret_cast<const int32_t*>(reset_meta_.as<char>() + (3 * nbuf + 1) * 8);
@@ -831,6 +832,7 @@ void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probe
     feed_raw_.ensure(chunk_floats * nbuf * sizeof(float));
     const size_t meta_stride = (slots.size() * 20 + 16 + 15) / 16 * 16;  // 8-B aligned offsets in each half
     feed_meta_.ensure(meta_stride * nbuf);
+    feed_meta_host_.ensure(meta_stride * nbuf);
     if (!feed_events_[0]) {
         cuda_check(cudaEventCreateWithFlags(&feed_events_[0], cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&feed_events_[1], cudaEventDisableTiming), "cudaEventCreate");
@@ -883,10 +885,11 @@ void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probe
         // of this chunk waits for them
         cuda_check(cudaStreamWaitEvent(copy_stream_, xpose_events_[buf], 0), "feed copy wait");
         cuda_check(cudaMemcpyAsync(raw, stage, at * sizeof(float), cudaMemcpyHostToDevice, copy_stream_), "feed H2D");
-        cuda_check(cudaMemcpyAsync(meta, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice, copy_stream_),
-                   "feed meta");
-        cuda_check(cudaMemcpyAsync(meta + offs.size() * 8, cols.data(), cols.size() * 4, cudaMemcpyHostToDevice,
-                                   copy_stream_),
+        // the metadata goes through pinned memory too, so no copy on copy_stream_ waits for the host
+        char* hmeta = feed_meta_host_.as<char>() + meta_stride * buf;
+        std::memcpy(hmeta, offs.data(), offs.size() * 8);
+        std::memcpy(hmeta + offs.size() * 8, cols.data(), cols.size() * 4);
+        cuda_check(cudaMemcpyAsync(meta, hmeta, offs.size() * 8 + cols.size() * 4, cudaMemcpyHostToDevice, copy_stream_),
                    "feed meta");
         cuda_check(cudaEventRecord(feed_events_[buf], copy_stream_), "feed event");
         cuda_check(cudaStreamWaitEvent(stream_, feed_events_[buf], 0), "feed wait");
@@ -910,7 +913,7 @@ void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probe
             const auto t0 = now();
             stage_chunk(c0, c1, i & 1);
             t_stage += std::chrono::duration<double>(now() - t0).count();
-            fused_->launch(c0, c1, NENG_STEP_EPILOGUE, stream_);
+            fused_->launch_chunk(c0, c1, stream_);
             ++last_launches_;
         }
     } else {
@@ -1130,6 +1133,7 @@ void Engine::run_device(int n_steps, const float* const* d_feeds, float* const* 
     device_call_args(n_steps, d_feeds, d_probes, &base, &present, &ring);
     launch_steps(n_steps, base, present, ring, stream);
     steps_done_ += n_steps;
+    last_run_steps_ = 0;  // the probe block no longer holds the engine's latest traces
 }
 
 void Engine::call_begin(int n_steps, const float* const* d_feeds, float* const* d_probes, cudaStream_t stream) {
@@ -1146,6 +1150,7 @@ void Engine::call_begin(int n_steps, const float* const* d_feeds, float* const* 
     fused_->begin(n_steps, base, feed_off.data(), present.data(), ring, ring_off.data(), stream);
     call_steps_ = n_steps;
     call_stream_ = stream;
+    last_run_steps_ = 0;  // the probe block no longer holds the engine's latest traces
     last_launches_ = 0;
 }
 
@@ -1172,8 +1177,11 @@ void Engine::shard_layout(int64_t* xbuf_floats, int64_t* rank_floats, float** xb
 void Engine::set_xhat_buffer(float* d_buf) {
     if (!fused_) throw RunError("set_xhat_buffer: the engine runs the generic interpreter");
     if (!d_buf) throw InvalidArgument("set_xhat_buffer: null buffer");
+    if (call_steps_) throw RunError("set_xhat_buffer: a stepped call is open");
     fused_->set_xhat_buffer(d_buf);
 }
+
+int Engine::last_schedule() const { return fused_ ? fused_->sched : (last_launches_ ? NENG_SCHED_GENERIC : 0); }
 
 void Engine::synchronize() { cuda_check(cudaStreamSynchronize(stream_), "synchronize"); }
 

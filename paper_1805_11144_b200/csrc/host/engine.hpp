@@ -88,6 +88,7 @@ class Engine {
     int mode() const { return mode_; }
     int requested_mode() const { return requested_mode_; }
     int64_t last_launches() const { return last_launches_; }
+    int last_schedule() const;
     const PlannedModel& planned() const { return pm_; }
     int num_probes() const { return static_cast<int>(pm_.model.probes.size()); }
     int probe_dim(int i) const { return static_cast<int>(pm_.model.signals[pm_.model.probes[i].signal].size()); }
@@ -160,7 +161,7 @@ class Engine {
     cudaEvent_t feed_events_[2] = {nullptr, nullptr};  // staging-buffer reuse (pipelined host feeds)
     cudaEvent_t xpose_events_[2] = {nullptr, nullptr};  // device raw-buffer reuse (transpose done)
     cudaStream_t copy_stream_ = nullptr;                 // feed H2D copies overlap the kernels
-    PinnedMem feed_stage_, probe_stage_;
+    PinnedMem feed_stage_, probe_stage_, feed_meta_host_;
 };
 
 }  // namespace nengb

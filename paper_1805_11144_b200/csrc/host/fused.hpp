@@ -16,6 +16,7 @@ class Engine;
 /// the planned model and advances whole steps with one grid barrier each.
 struct FusedPlan {
     virtual ~FusedPlan() = default;
+    int sched = 0;  // NENG_SCHED_* bits of the launches since the last begin()
     /// Advance n_steps; feed data [slot][n][dim][B] f32 (slots absent -> null
     /// entries), probe ring [probe][n][dim][B].  Returns kernel launches.
     virtual int64_t run(int n_steps, const float* d_feed_data, const int64_t* feed_off, const int* present,
@@ -33,6 +34,9 @@ struct FusedPlan {
     virtual void step(int k, int flags, cudaStream_t stream) = 0;
     // steps [k0, k1) of the open call in one launch (same flags as step)
     virtual void launch(int k0, int k1, int flags, cudaStream_t stream) = 0;
+    // steps [k0, k1) of the open call as one run()-style launch (epilogue
+    // included, barrier-free when the engine owns its xhat buffer)
+    virtual void launch_chunk(int k0, int k1, cudaStream_t stream) = 0;
     virtual void xhat_layout(int64_t* xbuf_floats, int64_t* rank_floats, float** xbuf) const = 0;
     virtual void set_xhat_buffer(float* d_buf) = 0;
 };

@@ -104,6 +104,7 @@ class FusedImpl : public FusedPlan {
             p.prof = d_prof.as<unsigned long long>();
         }
         d_work.ensure(16 + static_cast<size_t>(units) * 4);
+        sched = 0;
         p.work = d_work.as<int32_t>();
         p.done = p.work + 4;
         call = p;
@@ -119,6 +120,24 @@ class FusedImpl : public FusedPlan {
         p.first_update = (flags & NENG_STEP_FIRST_UPDATE) ? 1 : 0;
         p.epilogue = (flags & NENG_STEP_EPILOGUE) ? 1 : 0;
         cuda_check(cudaMemsetAsync(d_work.p, 0, 8, stream), "fused work reset");
+        sched |= NENG_SCHED_FUSED_STEPPED;
+        project(p, k0, k1, stream);
+        cuda_check(launch_fused(p, dmax, grid, k0, k1, stream), "fused kernel launch");
+    }
+
+    /// Steps [k0, k1) of the open call as one self-contained launch (the
+    /// previous launch's epilogue did step k0-1's connection updates): the
+    /// barrier-free schedule when the engine owns its xhat buffer, else one
+    /// grid barrier per step.  run() and the chunked host-buffer path of
+    /// Engine::run both advance through this.
+    void launch_chunk(int k0, int k1, cudaStream_t stream) override {
+        FusedProgram p = call;
+        p.first_update = 0;
+        p.epilogue = 1;
+        p.dataflow = dataflow ? 1 : 0;
+        cuda_check(cudaMemsetAsync(d_work.p, 0, dataflow ? 16 + static_cast<size_t>(units) * 4 : 8, stream),
+                   "fused work reset");
+        sched |= dataflow ? NENG_SCHED_FUSED_BARRIER_FREE : NENG_SCHED_FUSED_STEPPED;
         project(p, k0, k1, stream);
         cuda_check(launch_fused(p, dmax, grid, k0, k1, stream), "fused kernel launch");
     }
@@ -155,14 +174,7 @@ class FusedImpl : public FusedPlan {
         if (dataflow) K = std::max(1, std::min<int>(K, static_cast<int>((int64_t{1} << 30) / std::max(units, 1))));
         int64_t launches = 0;
         for (int k = 0; k < n_steps; k += K) {
-            FusedProgram p = call;
-            p.first_update = 0;
-            p.epilogue = 1;
-            p.dataflow = dataflow ? 1 : 0;
-            cuda_check(cudaMemsetAsync(d_work.p, 0, dataflow ? 16 + static_cast<size_t>(units) * 4 : 8, stream),
-                       "fused work reset");
-            project(p, k, std::min(n_steps, k + K), stream);
-            cuda_check(launch_fused(p, dmax, grid, k, std::min(n_steps, k + K), stream), "fused kernel launch");
+            launch_chunk(k, std::min(n_steps, k + K), stream);
             ++launches;
         }
         cuda_check(cudaStreamSynchronize(stream), "fused run");  // call tables are reused next call
@@ -288,6 +300,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         };
         std::vector<EnsInfo> ens;
         std::unordered_map<int, int> ens_of_in, ens_of_xhat;
+        std::unordered_map<int, std::pair<int, int>> ens_state_of;  // neuron signal -> (ensemble, FStateCap)
         for (int i = 0; i < nops; ++i) {
             const Operator& op = m.operators[i];
             if (op.kind != OpKind::SimNeurons) continue;
@@ -349,6 +362,10 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             for (double x : Ds.initial)
                 if (!std::isfinite(static_cast<float>(x))) fail("non-finite decoder weight");
             for (int o : {e.sn, e.enc, e.dec, e.rin, e.rj, e.rx}) claim(o);
+            ens_state_of[e.out] = {static_cast<int>(ens.size()), SC_OUT};
+            ens_state_of[e.v] = {static_cast<int>(ens.size()), SC_VOLTAGE};
+            ens_state_of[e.r] = {static_cast<int>(ens.size()), SC_REFRACTORY};
+            ens_state_of[e.j] = {static_cast<int>(ens.size()), SC_J};
             ens_of_in[e.in] = static_cast<int>(ens.size());
             ens_of_xhat[e.xhat] = static_cast<int>(ens.size());
             ens.push_back(std::move(e));
@@ -636,6 +653,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         // probes
         std::vector<FProbe> fp;
         std::vector<int> fp_ens;  // producing ensemble of each capture (-1: a fed node)
+        std::vector<std::vector<std::pair<int32_t, int32_t>>> scaps_of(fe.size());  // per ensemble (kind, probe)
         p.time_probe_step = p.time_probe_time = -1;
         for (size_t q = 0; q < m.probes.size(); ++q) {
             int s = m.probes[q].signal;
@@ -656,6 +674,9 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
                     fp.push_back(pr);
                     fp_ens.push_back(ens_of_xhat.count(s) ? ens_of_xhat.at(s) : -1);
                 }
+            } else if (ens_state_of.count(s)) {
+                const auto [ei, kind] = ens_state_of.at(s);
+                scaps_of[ei].push_back({kind, static_cast<int32_t>(q)});  // captured by the unit stepping it
             } else if (conn_of_filt.count(s)) {
                 FConn& x = fc[conn_of_filt[s]];
                 if (x.probe_filt >= 0) fail("two probes on one filtered value");
@@ -684,7 +705,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
 
         // barrier-free stepping tables: per-ensemble waits, destination-less
         // connections by source, xhat captures; the epilogue's connections
-        std::vector<int32_t> df_deps, df_orph, df_free, df_xp, df_dest;
+        std::vector<int32_t> df_deps, df_orph, df_free, df_xp, df_dest, sc_flat;
         std::vector<std::vector<int>> ens_srcs(fe.size()), ens_dsts(fe.size());
         {
             std::vector<std::vector<int>> orph(fe.size()), xps(fe.size());
@@ -724,6 +745,12 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
                 fe[e].xp_begin = static_cast<int32_t>(df_xp.size());
                 for (int q : xps[e]) df_xp.push_back(q);
                 fe[e].xp_count = static_cast<int32_t>(xps[e].size());
+                fe[e].sc_begin = static_cast<int32_t>(sc_flat.size() / 2);
+                for (auto [kind, q] : scaps_of[e]) {
+                    sc_flat.push_back(kind);
+                    sc_flat.push_back(q);
+                }
+                fe[e].sc_count = static_cast<int32_t>(scaps_of[e].size());
             }
         }
 
@@ -825,9 +852,13 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             const size_t n_order = order.size(), n_deps = df_deps.size(), n_orph = df_orph.size(),
                          n_xp = df_xp.size(), n_free = df_free.size();
             std::vector<int32_t> blob;
-            for (auto* v : {&order, &df_deps, &df_orph, &df_xp, &df_free, &df_dest}) blob.insert(blob.end(), v->begin(), v->end());
+            // the (kind, probe) pairs first: int2 loads need 8-B alignment
+            for (auto* v : {&sc_flat, &order, &df_deps, &df_orph, &df_xp, &df_free, &df_dest})
+                blob.insert(blob.end(), v->begin(), v->end());
             upload(impl->d_df, blob.data(), blob.size() * sizeof(int32_t));
             const int32_t* base = impl->d_df.as<int32_t>();
+            p.scaps = base;
+            base += sc_flat.size();
             p.order = base;
             p.deps = base + n_order;
             p.ens_orph = p.deps + n_deps;

@@ -902,6 +902,33 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
             __syncwarp();
             dn = 0;
         }
+        // probes on the ensemble's own neuron signals (capture_probes, exec.cpp:328-338):
+        // read back after the doubt queue has patched v, r and the spike bits
+        for (int c = 0; c < e.sc_count; ++c) {
+            const int2 cap = __ldg(reinterpret_cast<const int2*>(p.scaps) + e.sc_begin + c);
+            float* dst = p.ring + p.ring_off[cap.y] + static_cast<int64_t>(k) * e.n * B + b;
+            for (int i = n0; valid && i < n1; ++i) {
+                float val;
+                if (cap.x == SC_OUT) {
+                    val = (words[i] >> lane) & 1u ? e.amp_dt : 0.0f;
+                } else if (cap.x == SC_VOLTAGE || cap.x == SC_REFRACTORY) {
+                    val = vrow0[static_cast<int64_t>(i) * B + lane + (cap.x == SC_REFRACTORY ? rdelta : 0)];
+                } else {
+                    const float4* er = reinterpret_cast<const float4*>(S.E + i * DMAX);
+                    float a = 0.0f;
+#pragma unroll
+                    for (int q = 0; q < DMAX / 4; ++q) {
+                        const float4 w = er[q];
+                        a = a + w.x * x[4 * q];
+                        a = a + w.y * x[4 * q + 1];
+                        a = a + w.z * x[4 * q + 2];
+                        a = a + w.w * x[4 * q + 3];
+                    }
+                    val = S.bias[i] + a;
+                }
+                dst[static_cast<int64_t>(i) * B] = val;
+            }
+        }
         // the call's last step leaves J in the arena (DotInc(E, in, J) as above, once)
         if (last && valid) {
             for (int i = n0; i < n1; ++i) {

@@ -52,7 +52,13 @@ struct FEns {
     int32_t dep_begin, dep_count;    // (ensemble << 1) | lag: wait for done >= t - lag
     int32_t orph_begin, orph_count;  // destination-less connections this ensemble feeds
     int32_t xp_begin, xp_count;      // captures of this ensemble's xhat
+    int32_t sc_begin, sc_count;      // captures of its neuron state: (FStateCap kind, probe index) pairs in scaps
 };
+
+/// Probes on an ensemble's own per-neuron signals, captured by the unit that
+/// steps it (capture_probes, exec.cpp:328-338): the spike output, the voltage
+/// and refractory state after the step, and the input current J.
+enum FStateCap : int32_t { SC_OUT = 0, SC_VOLTAGE = 1, SC_REFRACTORY = 2, SC_J = 3 };
 
 struct FConn {
     int64_t src_base;  // arena base of the source signal (an ensemble's xhat or a fed node)
@@ -126,6 +132,7 @@ struct FusedProgram {
     const int32_t* deps = nullptr;      // FEns::dep_*
     const int32_t* ens_orph = nullptr;  // FEns::orph_*
     const int32_t* xprobes = nullptr;   // FEns::xp_*: indices into probes
+    const int32_t* scaps = nullptr;     // FEns::sc_*: (FStateCap, probe index) pairs
     const int32_t* free_orph = nullptr;   // destination-less connections from fed / constant sources
     int32_t n_free_orph = 0;
     const int32_t* dest_conns = nullptr;  // connections into an ensemble (the epilogue's)

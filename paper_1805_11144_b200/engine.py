@@ -21,6 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libneng_gpu.so")
 MODE_AUTO, MODE_GENERIC, MODE_FUSED = 0, 1, 2
 PRECISION_STRICT_FP32, PRECISION_TF32 = 0, 1
 STEP_FIRST_UPDATE, STEP_EPILOGUE = 1, 2
+SCHED_GENERIC, SCHED_FUSED_STEPPED, SCHED_BARRIER_FREE = 1, 2, 4  # neng_gpu_last_schedule bits
 
 _lib = None
 
@@ -57,6 +58,8 @@ def lib():
                    "neng_gpu_mode"):
             getattr(L, fn).argtypes = [P]
             getattr(L, fn).restype = C.c_int32
+        L.neng_gpu_last_schedule.argtypes = [P]
+        L.neng_gpu_last_schedule.restype = C.c_int32
         L.neng_gpu_last_launch_count.argtypes = [P]
         L.neng_gpu_last_launch_count.restype = C.c_int64
         L.neng_gpu_last_error.argtypes = [P]
@@ -198,3 +201,7 @@ class GpuEngine:
 
     def last_launch_count(self) -> int:
         return lib().neng_gpu_last_launch_count(self._h)
+
+    def last_schedule(self) -> int:
+        """NENG_SCHED_* bits of the most recent call (SCHED_BARRIER_FREE: the bench's kernel)."""
+        return lib().neng_gpu_last_schedule(self._h)

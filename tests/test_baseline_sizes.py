@@ -1,0 +1,149 @@
+"""Parity at the BASELINE.json sizes, through the exact kernels and schedules
+the bench times.
+
+* config 4 (2048 x 512 LIF, d=8, K=8, B=256): run_device, the barrier-free
+  fused kernel (fused_run_kernel<8, 256, PROF=0, DF=1> — the bench's `value`
+  leg), 200 steps; 8 sampled batch rows against solo reference engines
+  (rows are independent, test_exec.cpp:246-267): every probe bit-exact,
+  spike counts of 2,048 probed neurons, final v/r of probed ensembles.
+* config 4 through run() with host buffers (the bench's `e2e` leg): the
+  chunked feed staging keeps the barrier-free schedule.
+* config 2 (256 x 1024, d=16, B=32): the <16, 32, ...> instance.
+* config 3 (784-1024-1024-10, B=512, strict fp32): the generic executor.
+* config 1 (64-D circular convolution, B=64, 1000 steps): slow (planning).
+
+Bit-exact is stricter than the north star's tolerances (1e-4 relative on
+continuous signals, <= 1e-4 of neurons with a different spike count); the
+spike-count mismatch fraction is still computed and printed."""
+import numpy as np
+import pytest
+
+from oracle import refapi
+from paper_1805_11144_b200 import networks, passes
+from paper_1805_11144_b200.engine import MODE_FUSED, MODE_GENERIC, SCHED_BARRIER_FREE, SCHED_GENERIC, GpuEngine
+from tests.support.device import (add_probes, assert_f32_bitexact, device_feeds, device_ring, ring_rows,
+                                  solo_reference_rows, spike_count_mismatch)
+
+pytestmark = pytest.mark.gpu
+
+ROWS4 = (0, 37, 64, 101, 128, 177, 200, 255)
+
+
+def _ens_signal(model, label):
+    return next(s.id for s in model.signals if s.label == label)
+
+
+def _probe_ensembles(w, ens_out, ens_state):
+    """Spike probes on `ens_out`, voltage + refractory probes on `ens_state`."""
+    m = w.model
+    req = [(_ens_signal(m, f"ens{e}.out"), f"ens{e}.spikes") for e in ens_out]
+    for e in ens_state:
+        req += [(_ens_signal(m, f"ens{e}.voltage"), f"ens{e}.v"), (_ens_signal(m, f"ens{e}.refractory"), f"ens{e}.r")]
+    return add_probes(m, req)
+
+
+def _compare_rows(gpu_rows, refs, model, rows, context, spike_keys):
+    """gpu_rows: {key: [rows][steps][dim] f32}; refs: solo_reference_rows output."""
+    for i, b in enumerate(rows):
+        ref_out, _ = refs[i]
+        for k in ref_out:
+            assert_f32_bitexact(gpu_rows[k][i], ref_out[k][0], f"{context} row {b} probe {k}")
+    mism = [spike_count_mismatch(np.stack([gpu_rows[k][i] for i in range(len(rows))]),
+                                 np.stack([refs[i][0][k][0] for i in range(len(rows))])) for k in spike_keys]
+    frac = float(np.mean(mism)) if mism else 0.0
+    spikes = sum(int(np.count_nonzero(gpu_rows[k])) for k in spike_keys)
+    print(f"{context}: spike-count mismatch fraction {frac:.2e} over {len(rows)} rows "
+          f"({spikes} spikes in {len(spike_keys)} probed ensembles)")
+    assert frac <= 1e-4
+    return frac
+
+
+def test_config4_benchmarked_kernel_200_steps():
+    import torch
+    steps = 200
+    w = networks.config4(steps=steps)
+    spike_keys = _probe_ensembles(w, ens_out=(0, 1, 2, 3), ens_state=(7,))
+    pm = passes.run_passes(w.model)
+    gpu = GpuEngine(pm, w.batch)
+    assert gpu.mode() == MODE_FUSED
+    dev = torch.device("cuda", 0)
+    feeds, fptrs = device_feeds(w, steps, dev)
+    ring, rptrs, offs = device_ring(pm.model, steps, w.batch, dev)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        gpu.run_device(steps, fptrs, rptrs, stream.cuda_stream)
+    stream.synchronize()
+    assert gpu.last_schedule() == SCHED_BARRIER_FREE  # the bench's kernel, no per-step barrier
+    assert gpu.last_launch_count() == 1
+    got = ring_rows(ring, offs, pm.model, steps, w.batch, ROWS4)
+    state = [_ens_signal(pm.model, f"ens{e}.{s}") for e in (7, 1500) for s in ("voltage", "refractory")]
+    refs = solo_reference_rows(refapi, pm, w.feeds, ROWS4, steps, signals=state)
+    _compare_rows(got, refs, pm.model, ROWS4, "config4 run_device", spike_keys)
+    for i, b in enumerate(ROWS4):
+        for s in state:
+            g, r = gpu.read_signal(s, b), refs[i][1][s]
+            assert np.array_equal(g.view(np.uint64), r.view(np.uint64)), f"row {b} signal {s}"
+
+
+def test_config4_host_buffers_keep_the_barrier_free_schedule():
+    # the e2e leg: run() with host f64 feeds stages them in chunks of 4, 8, 16, 32 steps;
+    # each chunk is one barrier-free launch
+    steps = 40
+    w = networks.config4(steps=steps)
+    spike_keys = _probe_ensembles(w, ens_out=(5,), ens_state=())
+    pm = passes.run_passes(w.model)
+    gpu = GpuEngine(pm, w.batch)
+    out = gpu.run(steps, w.feeds)
+    assert gpu.last_schedule() == SCHED_BARRIER_FREE
+    assert gpu.last_launch_count() > 1  # chunked
+    rows = (3, 250)
+    refs = solo_reference_rows(refapi, pm, w.feeds, rows, steps)
+    got = {k: out[k][list(rows)].astype(np.float32) for k in out}
+    _compare_rows(got, refs, pm.model, rows, "config4 run()", spike_keys)
+
+
+def test_config2_full_batch():
+    steps = 100
+    w = networks.config2(steps=steps)
+    spike_keys = _probe_ensembles(w, ens_out=(0, 200), ens_state=(9,))
+    pm = passes.run_passes(w.model)
+    gpu = GpuEngine(pm, w.batch)
+    assert gpu.mode() == MODE_FUSED
+    out = gpu.run(steps, w.feeds)
+    assert gpu.last_schedule() == SCHED_BARRIER_FREE
+    rows = (0, 5, 11, 16, 21, 26, 30, 31)
+    refs = solo_reference_rows(refapi, pm, w.feeds, rows, steps)
+    got = {k: out[k][list(rows)].astype(np.float32) for k in out}
+    _compare_rows(got, refs, pm.model, rows, "config2 B=32", spike_keys)
+
+
+def test_config3_strict_full_batch():
+    steps = 100
+    w = networks.config3(steps=steps)
+    m = w.model
+    spike_keys = add_probes(m, [(_ens_signal(m, "l1.out"), "l1.spikes"), (_ens_signal(m, "l2.out"), "l2.spikes")])
+    pm = passes.run_passes(m)
+    gpu = GpuEngine(pm, w.batch)
+    assert gpu.mode() == MODE_GENERIC
+    out = gpu.run(steps, w.feeds)
+    assert gpu.last_schedule() == SCHED_GENERIC
+    rows = (0, 73, 146, 219, 292, 365, 438, 511)
+    refs = solo_reference_rows(refapi, pm, w.feeds, rows, steps)
+    got = {k: out[k][list(rows)].astype(np.float32) for k in out}
+    _compare_rows(got, refs, pm.model, rows, "config3 B=512 strict", spike_keys)
+
+
+@pytest.mark.slow
+def test_config1_full_size_1000_steps():
+    # 64-D circular convolution, B=64, 1000 steps (35k operators, 142 plan groups)
+    w = networks.config1(steps=1000, batch=64, dims=64)
+    pm = passes.run_passes(w.model)
+    gpu = GpuEngine(pm, w.batch)
+    out = gpu.run(w.steps, w.feeds)
+    ref = refapi.RefEngine(pm, w.batch)
+    r = ref.run(w.steps, w.feeds)
+    for k in r:
+        assert_f32_bitexact(out[k].astype(np.float32), r[k], f"config1 probe {k}")
+    for s in pm.model.signals[::37]:
+        for b in (0, w.batch - 1):
+            assert np.array_equal(gpu.read_signal(s.id, b).view(np.uint64), ref.read_signal(s.id, b).view(np.uint64))

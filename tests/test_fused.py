@@ -6,7 +6,9 @@ import pytest
 
 from oracle import refapi
 from paper_1805_11144_b200 import networks, passes
-from paper_1805_11144_b200.engine import MODE_FUSED, MODE_GENERIC, GpuEngine
+from paper_1805_11144_b200.engine import (MODE_FUSED, MODE_GENERIC, SCHED_BARRIER_FREE, SCHED_FUSED_STEPPED,
+                                          GpuEngine)
+from tests.support.device import device_feeds, device_ring
 from tests.support.models import assert_bitexact, batch_slice, step_slice
 
 pytestmark = pytest.mark.gpu
@@ -92,33 +94,6 @@ def test_config4_full_batch_sampled_rows_bit_exact():
                 f"row {b} signal {s.label}"
 
 
-def _device_feeds(w, steps, dev):
-    """w.feeds ([batch][steps][dim] f64 per node) as one packed [slot][step][dim][B] f32 block."""
-    import torch
-    blocks = []
-    for fs in w.model.feed_slots:
-        f = w.feeds[fs.node_id][:, :steps, :]
-        blocks.append(torch.as_tensor(np.ascontiguousarray(f.transpose(1, 2, 0)), dtype=torch.float32).reshape(-1))
-    flat = torch.cat(blocks).to(dev) if blocks else torch.zeros(1, device=dev)
-    ptrs, at = [], 0
-    for fs in w.model.feed_slots:
-        ptrs.append(flat.data_ptr() + 4 * at)
-        at += steps * fs.dim * w.batch
-    return flat, ptrs
-
-
-def _device_ring(model, steps, batch, dev):
-    import torch
-    dims = [model.signals[p.signal].size() for p in model.probes]
-    ring = torch.full((max(sum(dims) * steps * batch, 1),), float("nan"), device=dev)
-    ptrs, offs, at = [], [], 0
-    for d in dims:
-        ptrs.append(ring.data_ptr() + 4 * at)
-        offs.append((at, d * steps * batch))
-        at += d * steps * batch
-    return ring, ptrs, offs
-
-
 def test_two_ensemble_shards_match_the_unsharded_engine():
     # two shards of one network driven on one GPU (their launches never wait on each other;
     # the "all-gather" is a copy of each shard's xhat rows into the other's parity buffer)
@@ -138,15 +113,15 @@ def _two_shards_on_one_stream(pm, w, n, B, dev, stream):
     import torch
     from paper_1805_11144_b200.engine import STEP_EPILOGUE, STEP_FIRST_UPDATE
     from paper_1805_11144_b200.shard import attach_xhat_buffer
-    feeds, fptrs = _device_feeds(w, n, dev)
+    feeds, fptrs = device_feeds(w, n, dev)
 
     whole = GpuEngine(pm, B)
-    ring_w, rptrs_w, offs = _device_ring(pm.model, n, B, dev)
+    ring_w, rptrs_w, offs = device_ring(pm.model, n, B, dev)
     whole.run_device(n, fptrs, rptrs_w, stream)
 
     shards = [GpuEngine(pm, B, shard=(r, 2)) for r in range(2)]
     xb = [attach_xhat_buffer(s, dev) for s in shards]
-    rings = [_device_ring(pm.model, n, B, dev) for _ in shards]
+    rings = [device_ring(pm.model, n, B, dev) for _ in shards]
     for s, (ring, rptrs, _) in zip(shards, rings):
         s.call_begin(n, fptrs, rptrs, stream)
     rf = xb[0][1]
@@ -243,6 +218,8 @@ def test_captures_and_orphans_both_schedules(dataflow, monkeypatch):
         ref = refapi.RefEngine(pm, w.batch)
         for i, (n, f) in enumerate(calls):
             assert_bitexact(gpu.run(n, f), ref.run(n, f), f"dataflow={dataflow} spl={spl} call {i}")
+            # fed calls longer than 4 steps stage their feeds in chunks: each chunk keeps the schedule
+            assert gpu.last_schedule() == (SCHED_BARRIER_FREE if dataflow == "1" else SCHED_FUSED_STEPPED)
             full_state_equal(gpu, ref, pm.model, w.batch, f"dataflow={dataflow} spl={spl} call {i}")
 
 
@@ -273,3 +250,26 @@ def test_wide_fed_connections_projected_ahead_of_the_kernel():
     full_state_equal(gpu, ref, pm.model, w.batch, "projected feeds")
     assert_bitexact(gpu.run(7), ref.run(7), "default node values")
     full_state_equal(gpu, ref, pm.model, w.batch, "default node values")
+
+
+@pytest.mark.parametrize("dataflow", ["1", "0"])
+def test_neuron_state_probes_stay_fused(dataflow, monkeypatch):
+    # probes on an ensemble's spikes, voltage, refractory state and input current are
+    # captured by the unit that steps it (the fused pipeline keeps the graph)
+    monkeypatch.setenv("NENG_FUSED_DATAFLOW", dataflow)
+    w = networks.random_network(13, n_ens=6, n=80, d=4, k_out=2, n_inputs=3, batch=40, steps=19)
+    m = w.model
+    lab = {s.label: s.id for s in m.signals}
+    from tests.support.device import add_probes
+    add_probes(m, [(lab["ens1.out"], "spikes"), (lab["ens1.voltage"], "v"), (lab["ens2.refractory"], "r"),
+                   (lab["ens3.J"], "J"), (lab["ens1.out"], "spikes again")])
+    pm = passes.run_passes(m)
+    gpu = GpuEngine(pm, w.batch)
+    assert gpu.mode() == MODE_FUSED
+    ref = refapi.RefEngine(pm, w.batch)
+    for i, (a, n) in enumerate(((0, 12), (12, 7))):
+        f = step_slice(w.feeds, a, n)
+        out = gpu.run(n, f)
+        assert_bitexact(out, ref.run(n, f), f"state probes call {i}")
+        assert np.count_nonzero(out[pm.model.probes[-5].key]) > 0  # the spike probe saw spikes
+    full_state_equal(gpu, ref, pm.model, w.batch, "state probes")
