@@ -12,8 +12,13 @@ minibatch.  `value` is device-timed (CUDA events on the launching stream, all
 feeds resident in HBM, one persistent launch for the K timed steps); `e2e` is
 the same metric through the C ABI entry neng_gpu_run with host f64 feeds and
 host f64 probe outputs (H2D/D2H inside the timed region).  Multi-GPU: one
-process per GPU, each rank simulates its own 256-row minibatch of the same
-network (weak scaling, no collective on the data path); time = max over ranks.
+process per GPU.  Default (`--shard batch --scaling strong`): the north
+star's minibatch sharding — the global minibatch of 256 rows is split into
+256/N rows per GPU, each rank simulates its rows of the same network with no
+collective on the data path (batch rows are independent, test_exec.cpp:246-267).
+`--scaling weak` keeps 256 rows per GPU (N replicas).  `--shard ensemble`
+splits the ensembles instead, with a per-step NCCL all-gather of the decoded
+outputs.  Time = max over ranks.
 """
 from __future__ import annotations
 
@@ -44,6 +49,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="--shard batch: 'strong' splits the global minibatch (--batch) into batch/N rows per GPU; "
+                         "'weak' runs --batch rows on every GPU")
     ap.add_argument("--shard", choices=["batch", "ensemble"], default="batch",
                     help="multi-GPU mode: 'batch' = one minibatch replica per GPU (weak scaling, no collective); "
                          "'ensemble' = the ensembles split across GPUs with a per-step NCCL all-gather of the "
@@ -112,9 +120,18 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def build_workload(args, rank):
+def rows_per_rank(args, world):
+    """Minibatch rows this rank simulates."""
+    if args.shard == "batch" and args.scaling == "strong":
+        if args.batch % world:
+            raise SystemExit(f"--batch {args.batch} does not split over {world} GPUs")
+        return args.batch // world
+    return args.batch
+
+
+def build_workload(args, rank, rows):
     from paper_1805_11144_b200 import networks, passes
-    w = networks.random_network(args.seed, 2048, 512, 8, 8, 256, args.batch, 1, name="config4_random_2048x512")
+    w = networks.random_network(args.seed, 2048, 512, 8, 8, 256, rows, 1, name="config4_random_2048x512")
     t0 = time.time()
     pm = passes.run_passes(w.model)
     plan_s = time.time() - t0
@@ -146,7 +163,7 @@ def run_reference_arm(args):
     if rank != 0:
         return
     from paper_1805_11144_b200 import networks
-    w, pm, _ = build_workload(args, rank)
+    w, pm, _ = build_workload(args, rank, args.batch)
     neurons = networks.neuron_count(w.model)
     from oracle import refapi
     threads = os.cpu_count() or 1
@@ -180,8 +197,9 @@ def main():
     from paper_1805_11144_b200 import networks
     from paper_1805_11144_b200.engine import GpuEngine
 
-    w, pm, plan_s = build_workload(args, rank)
+    w, pm, plan_s = build_workload(args, rank, rows_per_rank(args, world))
     B = w.batch
+    split = args.shard == "batch" and args.scaling == "strong"
     neurons = networks.neuron_count(w.model)
     bytes_step = networks.algorithmic_bytes_per_step(w.model, B)
     sharded = args.shard == "ensemble"
@@ -253,8 +271,9 @@ def main():
         ms = float(t.item())
         torch.distributed.barrier()
     steps_per_s = K / (ms / 1e3)
-    # batch sharding: every rank advances its own minibatch; ensemble sharding: one minibatch in total
-    value = steps_per_s * neurons * B * (1 if sharded else world)
+    # batch sharding: every rank advances its own B rows; ensemble sharding: one minibatch in total
+    global_b = B if sharded else B * world
+    value = steps_per_s * neurons * global_b
 
     # end to end through the C ABI with host buffers (f64 feeds in, f64 probes out)
     e2e = None
@@ -276,7 +295,7 @@ def main():
             sec = float(t.item())
         h2d = sum(fs.dim for fs in slots) * B * 4
         d2h = sum(w.model.signals[p.signal].size() for p in w.model.probes) * B * 4
-        e2e = {"value": Ke / sec * neurons * B * world, "unit": UNIT, "h2d_bytes_per_step": h2d,
+        e2e = {"value": Ke / sec * neurons * global_b, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": Ke,
                "note": "neng_gpu_run: host f64 feeds -> f32 staging -> H2D -> fused kernel -> probe D2H -> f64"}
 
@@ -297,12 +316,13 @@ def main():
         pass
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong" if (sharded or split) else "weak",
         "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": "config4_random_2048x512", "neurons": neurons, "batch_per_gpu": B,
-                   "global_batch": B * (1 if sharded else world),
+                   "global_batch": global_b,
                    "parallelism": (f"ensemble shards x{world} (per-step NCCL all-gather of xhat)" if sharded
+                                   else f"minibatch split x{world} ({B} rows per GPU, no collective)" if split
                                    else f"minibatch replicas x{world}"),
                    "ensembles": 2048, "neurons_per_ensemble": 512, "dims": 8, "out_connections": 8,
                    "inputs": 256, "operators": len(pm.model.operators), "groups_per_step": len(pm.plan),

@@ -85,6 +85,30 @@ def test_config4_benchmarked_kernel_200_steps():
             assert np.array_equal(g.view(np.uint64), r.view(np.uint64)), f"row {b} signal {s}"
 
 
+def test_config4_per_gpu_slice_of_the_8_gpu_split():
+    # bench.py --gpus 8 (default minibatch split): each GPU runs 256/8 = 32 rows through
+    # run_device, the <8, 32, 0, 1> instance (one tile per unit, warps slice the neurons)
+    import torch
+    steps = 120
+    w = networks.config4(steps=steps, batch=32)
+    spike_keys = _probe_ensembles(w, ens_out=(11, 1999), ens_state=(3,))
+    pm = passes.run_passes(w.model)
+    gpu = GpuEngine(pm, w.batch)
+    assert gpu.mode() == MODE_FUSED
+    dev = torch.device("cuda", 0)
+    feeds, fptrs = device_feeds(w, steps, dev)
+    ring, rptrs, offs = device_ring(pm.model, steps, w.batch, dev)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        gpu.run_device(steps, fptrs, rptrs, stream.cuda_stream)
+    stream.synchronize()
+    assert gpu.last_schedule() == SCHED_BARRIER_FREE
+    rows = (0, 9, 17, 31)
+    got = ring_rows(ring, offs, pm.model, steps, w.batch, rows)
+    refs = solo_reference_rows(refapi, pm, w.feeds, rows, steps)
+    _compare_rows(got, refs, pm.model, rows, "config4 B=32 run_device", spike_keys)
+
+
 def test_config4_host_buffers_keep_the_barrier_free_schedule():
     # the e2e leg: run() with host f64 feeds stages them in chunks of 4, 8, 16, 32 steps;
     # each chunk is one barrier-free launch
