@@ -103,6 +103,17 @@ class FusedImpl : public FusedPlan {
             cuda_check(cudaMemsetAsync(d_prof.p, 0, (FS_COUNT + 4) * 8, stream), "profile reset");
             p.prof = d_prof.as<unsigned long long>();
         }
+        p.trace = nullptr;
+        if (std::getenv("NENG_FUSED_TRACE") != nullptr) {  // fault localisation (-DNENG_FUSED_TRACE builds)
+            const size_t words = static_cast<size_t>(grid) * 8 * 2;
+            if (!trace_host) {
+                cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&trace_host), words * 4, cudaHostAllocMapped),
+                           "trace alloc");
+                cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&trace_dev), trace_host, 0), "trace map");
+            }
+            std::memset(trace_host, 0, words * 4);
+            p.trace = trace_dev;
+        }
         d_work.ensure(16 + static_cast<size_t>(units) * 4);
         sched = 0;
         p.work = d_work.as<int32_t>();
@@ -123,6 +134,7 @@ class FusedImpl : public FusedPlan {
         sched |= NENG_SCHED_FUSED_STEPPED;
         project(p, k0, k1, stream);
         cuda_check(launch_fused(p, dmax, grid, k0, k1, stream), "fused kernel launch");
+        trace_check(stream);
     }
 
     /// Steps [k0, k1) of the open call as one self-contained launch (the
@@ -140,6 +152,21 @@ class FusedImpl : public FusedPlan {
         sched |= dataflow ? NENG_SCHED_FUSED_BARRIER_FREE : NENG_SCHED_FUSED_STEPPED;
         project(p, k0, k1, stream);
         cuda_check(launch_fused(p, dmax, grid, k0, k1, stream), "fused kernel launch");
+        trace_check(stream);
+    }
+
+    int32_t* trace_host = nullptr;
+    int32_t* trace_dev = nullptr;
+    /// NENG_FUSED_TRACE: wait for the launch; on a fault print every warp's last checkpoint
+    void trace_check(cudaStream_t stream) {
+        if (!call.trace) return;
+        if (cudaStreamSynchronize(stream) == cudaSuccess) return;
+        for (int c = 0; c < grid; ++c) {
+            std::fprintf(stderr, "[fused trace] cta %d:", c);
+            for (int w = 0; w < 8; ++w)
+                std::fprintf(stderr, " %d/%d", trace_host[2 * (c * 8 + w)], trace_host[2 * (c * 8 + w) + 1]);
+            std::fprintf(stderr, "\n");
+        }
     }
 
     /// the fed-node projections of steps [k0, k1) (before the launch that reads them)
@@ -189,7 +216,7 @@ class FusedImpl : public FusedPlan {
             for (int s = 0; s < FS_COUNT; ++s)
                 std::fprintf(stderr, " %s=%.1f", names[s], h[s] / 1e3 / grid / n_steps);
             std::fprintf(stderr, " (total %.1f)\n", tot / 1e3 / grid / n_steps);
-            std::fprintf(stderr, "[fused profile] per step: doubt entries %.0f, exact path %.0f\n",
+            std::fprintf(stderr, "[fused profile] per step: queued transcendental lane evaluations %.0f, exact path %.0f\n",
                          double(h[FS_COUNT]) / n_steps, double(h[FS_COUNT + 1]) / n_steps);
         }
         return launches;

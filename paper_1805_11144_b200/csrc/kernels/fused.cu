@@ -102,6 +102,22 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) 
 __device__ __forceinline__ void prefetch_l2_line(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
+#ifdef NENG_FUSED_TRACE
+#define FTRACE(cp, val)                                                                             \
+    do {                                                                                           \
+        if (p.trace && (threadIdx.x & 31) == 0) {                                                  \
+            volatile int32_t* t_ = p.trace + 2 * (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); \
+            t_[0] = (cp);                                                                          \
+            t_[1] = (val);                                                                         \
+            __threadfence_system();                                                                \
+        }                                                                                          \
+    } while (0)
+#else
+#define FTRACE(cp, val) \
+    do {                \
+    } while (0)
+#endif
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -141,12 +157,14 @@ struct Ticker {
     }
 };
 
+/// A queued neuron step (exception queues, see run_unit): key = neuron << 5 | lane.
+///   exit queue  (the step leaving the refractory period): a, b, c = the step's v, r, J
+///   spike queue (a spike; v = 0 is already stored):       a, b    = the pre-reset voltage, J
 struct __align__(16) QEnt {
-    uint32_t key;  // neuron << 5 | lane, | kDoubtExp / kDoubtLog: which speculative value was doubtful
-    float a, b, c; // the step's original v, r, J
+    uint32_t key;
+    float a, b, c;
 };
-constexpr uint32_t kDoubtExp = 0x80000000u, kDoubtLog = 0x40000000u;
-constexpr int kDQ = 64;  // per-warp doubt queue: <= 31 pending + 32 from a neuron row
+constexpr int kQ = 64;  // per-warp queue capacity: <= 31 pending + 32 from a row (drained at >= 32)
 
 struct Smem {
     uint64_t* bar;
@@ -155,21 +173,22 @@ struct Smem {
     float* E;      // nmax x DMAX (zero padded)
     float* bias;   // nmax
     float* P;      // decoder products [n][dx] (when p.stage_dec)
-    float* in;     // tu x DMAX x 32
+    float* in;     // tu x DMAX x 32 (aliases the queues: read into registers before the sweep)
     uint32_t* words;  // tu x nmax: spike ballot of neuron i in tile slot t (bit = lane)
     float* ring;      // kWarps x [2 stages][v, r][kUnroll rows][32]
-    QEnt* dq;         // kWarps x kDQ doubt entries
-    uint8_t* w8e;     // byte screening windows per region (expm1, log1p), see libm_w8_bytes
-    uint8_t* w8l;
+    QEnt* qe;         // kWarps x kQ exit-queue entries
+    QEnt* qs;         // kWarps x kQ spike-queue entries
 };
 
-/// Bytes of one shared-memory copy of a region byte table (rounded to 16).
-__host__ __device__ __forceinline__ size_t libm_w8_bytes(const LibmTables& t) {
-    return (static_cast<size_t>(t.t[0].n_regions > t.t[1].n_regions ? t.t[0].n_regions : t.t[1].n_regions) + 15) &
-           ~static_cast<size_t>(15);
-}
-
 constexpr int kRingFloats = 2 * 2 * kUnroll * 32;  // per warp
+constexpr size_t kQueueBytes = 2 * sizeof(QEnt) * kQ * kWarps;
+
+/// Bytes of the region shared by the input staging `in` and the queues.
+template <int DMAX>
+__host__ __device__ __forceinline__ size_t inq_bytes(const FusedProgram& p) {
+    const size_t in = static_cast<size_t>(p.tu) * DMAX * 32 * 4;
+    return in > kQueueBytes ? in : kQueueBytes;
+}
 
 template <int DMAX>
 __device__ Smem carve(uint32_t* base, const FusedProgram& p) {
@@ -181,20 +200,16 @@ __device__ Smem carve(uint32_t* base, const FusedProgram& p) {
     at += 128;
     S.ring = reinterpret_cast<float*>(at);
     at += static_cast<size_t>(kWarps) * kRingFloats * 4;
-    S.dq = reinterpret_cast<QEnt*>(at);
-    at += sizeof(QEnt) * kDQ * kWarps;
-    S.w8e = reinterpret_cast<uint8_t*>(at);
-    at += libm_w8_bytes(p.libm);
-    S.w8l = reinterpret_cast<uint8_t*>(at);
-    at += libm_w8_bytes(p.libm);
+    S.qe = reinterpret_cast<QEnt*>(at);
+    S.qs = S.qe + kQ * kWarps;
+    S.in = reinterpret_cast<float*>(at);
+    at += inq_bytes<DMAX>(p);
     S.E = reinterpret_cast<float*>(at);
     at += static_cast<size_t>(p.nmax) * DMAX * 4;
     S.bias = reinterpret_cast<float*>(at);
     at += static_cast<size_t>(p.nmax) * 4;
     S.P = reinterpret_cast<float*>(at);
     at += static_cast<size_t>(p.stage_dec ? p.pmax_floats : 0) * 4;
-    S.in = reinterpret_cast<float*>(at);
-    at += static_cast<size_t>(p.tu) * DMAX * 32 * 4;
     S.words = reinterpret_cast<uint32_t*>(at);
     at += static_cast<size_t>(p.tu) * p.nmax * 4;
     return S;
@@ -202,10 +217,9 @@ __device__ Smem carve(uint32_t* base, const FusedProgram& p) {
 
 template <int DMAX>
 size_t smem_bytes(const FusedProgram& p) {
-    return 128 + static_cast<size_t>(kWarps) * kRingFloats * 4 + 2 * libm_w8_bytes(p.libm) + sizeof(QEnt) * kDQ * kWarps +
-           static_cast<size_t>(p.nmax) * DMAX * 4 +
-           static_cast<size_t>(p.nmax) * 4 + static_cast<size_t>(p.stage_dec ? p.pmax_floats : 0) * 4 +
-           static_cast<size_t>(p.tu) * DMAX * 32 * 4 + static_cast<size_t>(p.tu) * p.nmax * 4;
+    return 128 + static_cast<size_t>(kWarps) * kRingFloats * 4 + inq_bytes<DMAX>(p) +
+           static_cast<size_t>(p.nmax) * DMAX * 4 + static_cast<size_t>(p.nmax) * 4 +
+           static_cast<size_t>(p.stage_dec ? p.pmax_floats : 0) * 4 + static_cast<size_t>(p.tu) * p.nmax * 4;
 }
 
 /// The batch width: BT when the kernel is specialised for it (row strides then
@@ -218,102 +232,32 @@ __device__ __forceinline__ int batch_of(const FusedProgram& p) {
         return p.batch;
 }
 
-/// Warp-aggregated push: lanes with `pred` append `e` in lane order; returns the new count.
-__device__ __forceinline__ int qpush(QEnt* q, int n, bool pred, const QEnt& e) {
-    const uint32_t m = __ballot_sync(kFull, pred);
-    if (pred) q[n + __popc(m & lanemask_lt())] = e;
-    return n + __popc(m);
-}
-
-// ---- async row copies (cp.async, LDGSTS) ------------------------------------
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-// L2 policies: the streamed neuron state is evict-first, so the libm tables the
-// doubt resolution probes (a few MB) stay L2-resident next to 2 GB/step of v, r
+// L2 policy: the streamed neuron state is evict-first, so the libm tables the
+// queue batches probe (a few MB) stay L2-resident next to 2 GB/step of v, r
 __device__ __forceinline__ uint64_t l2_evict_first() {
     uint64_t pol;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
-__device__ __forceinline__ uint64_t l2_evict_last() {
-    uint64_t pol;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
+// No L2::cache_hint operand on cp.async: for some kernel shapes (the BT = 0
+// instances) ptxas 12.9 encodes the hinted LDGSTS with its 64-bit memory
+// descriptor in an odd uniform register (desc[UR1]), which faults at run time
+// with "illegal instruction"; tests/test_abi.py scans the SASS for it.
 __device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-                 "l"(l2_evict_first())
-                 : "memory");
-}
-__device__ __forceinline__ uint32_t ldg_keep(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(l2_evict_last()));
-    return v;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async4_s(uint32_t dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
 }
 
-/// A lane's share of the ring copies, precomputed once per sweep.  vec (B % 4
-/// == 0): lane copies 16 B, columns c4..c4+3 of rows (lane >> 3) and
-/// (lane >> 3) + 4 of each 8-row round; else 4 B (its own column) of all 8 rows.
-struct RingLane {
-    const float* src;  // v element (row n0 + lane-row, column b0 + lane-col)
-    int64_t rdelta;    // r_base - v_base
-    uint32_t dst;      // shared address of the lane's first element in stage 0
-    int row;           // first row of the round this lane copies
-    bool ok;           // the lane's columns exist
-};
-
-/// Copy the round starting at row i (rows below n1) of v and r into stage st.
-template <int BT>
-__device__ __forceinline__ void ring_issue(const RingLane& L, int st, int i, int n0, int n1, int B, bool vec) {
-    const int64_t Bs = BT > 0 ? BT : B;
-    const float* src = L.src + static_cast<int64_t>(i - n0) * Bs;
-    const uint32_t dst = L.dst + st * (kUnroll * 32 * 4);
-    if (L.ok) {
-        if (vec) {
-#pragma unroll
-            for (int h = 0; h < kUnroll / 4; ++h)
-                if (i + L.row + 4 * h < n1) {
-                    cp_async16_s(dst + h * 4 * 32 * 4, src + 4 * h * Bs);
-                    cp_async16_s(dst + h * 4 * 32 * 4 + 2 * kUnroll * 32 * 4, src + 4 * h * Bs + L.rdelta);
-                }
-        } else {
-#pragma unroll
-            for (int rr = 0; rr < kUnroll; ++rr)
-                if (i + rr < n1) {
-                    cp_async4_s(dst + rr * 32 * 4, src + rr * Bs);
-                    cp_async4_s(dst + rr * 32 * 4 + 2 * kUnroll * 32 * 4, src + rr * Bs + L.rdelta);
-                }
-        }
-    }
-    cp_async_commit();
-}
-
-/// The speculative LIF-range evaluation of libm.cuh (spec_expm1 / spec_log1p)
-/// with the per-region screen read from the shared-memory byte table:
+/// The speculative LIF-range evaluation of libm.cuh (expm1_fast / log1p_fast)
+/// with the per-region screen read from the byte table (8 KB, L1-resident):
 /// doubtful when |low29 - 2^28| >> 21 <= w8 (a superset of the exact window,
-/// so every value the exact screen flags is flagged here too).
-__device__ __forceinline__ Spec spec_smem(float x, bool is_log, const uint8_t* w8, uint32_t shift) {
-    const double y = is_log ? log1p_fast(static_cast<double>(x)) : expm1_fast(static_cast<double>(x));
-    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(y));
-    const uint32_t hi = static_cast<uint32_t>(u >> 32), lo = static_cast<uint32_t>(u);
-    const bool den = (hi & 0x7FF00000u) < (897u << 20);  // |y| < 2^-126: float-denormal result
-    const uint32_t d = static_cast<uint32_t>(abs(static_cast<int>(lo & 0x1FFFFFFFu) - 0x10000000));
-    const uint32_t w = w8[(__float_as_uint(x) - 0x80000000u) >> shift];
-    return {static_cast<float>(y), den || (d >> 21) <= w};
-}
-
-/// spec_smem for any x: `doubtful` also when x is outside the LIF range (the
-/// polynomial is then meaningless and the exact path takes over).
+/// so every value the exact screen flags is flagged here too), when the result
+/// is a float denormal, or when x is outside the LIF range [-1/16, 0).
 __device__ __forceinline__ Spec spec_any(float x, bool is_log, const uint8_t* w8, uint32_t shift) {
     const uint32_t k = __float_as_uint(x) - 0x80000001u;  // x in [-1/16, 0) <=> k <= 0x3D7FFFFF
     const bool inr = k <= 0x3D7FFFFFu;
@@ -322,21 +266,74 @@ __device__ __forceinline__ Spec spec_any(float x, bool is_log, const uint8_t* w8
     const uint32_t hi = static_cast<uint32_t>(u >> 32), lo = static_cast<uint32_t>(u);
     const bool den = (hi & 0x7FF00000u) < (897u << 20);  // |y| < 2^-126: float-denormal result
     const uint32_t d = static_cast<uint32_t>(abs(static_cast<int>(lo & 0x1FFFFFFFu) - 0x10000000));
-    const uint32_t w = w8[min(k + 1u, 0x3D800000u) >> shift];
+    const uint32_t w = __ldg(w8 + (min(k + 1u, 0x3D800000u) >> shift));
     return {static_cast<float>(y), !inr || den || (d >> 21) <= w};
 }
 
-/// lif_spike_step<float> resolved exactly (table probes as needed); returns
-/// whether the neuron spiked.
-__device__ __forceinline__ bool lif_exact(float J, float& v, float& r, float dt, float tau_rc, float tau_ref,
-                                          const LibmTables& t) {
+/// glibc's value of expm1f / log1pf (is_log) at x on the LIF range, without the
+/// slow paths: the rounded polynomial unless it is doubtful and x is listed in
+/// the bucketed table (then the table value).  Returns false when only the
+/// exact path can decide (x outside the LIF range, or a full bucket).  The
+/// table pointers come from the kernel parameters (constant bank), so nothing
+/// of this stays live in registers across the sweep.
+__device__ __forceinline__ bool glibc_fast(float x, bool is_log, const LibmTables& lt, float* out) {
+    const LibmHash& h = lt.t[is_log ? 1 : 0];
+    const Spec sp = spec_any(x, is_log, h.region_w8, h.region_shift);
+    *out = sp.r;
+    if (!sp.doubtful) return true;
+    const uint32_t ka = __float_as_uint(x);
+    if (ka - 0x80000001u > 0x3D7FFFFFu) return false;  // outside the LIF range
+    const uint32_t bi = (ka * 0x9E3779B1u) >> h.bucket_shift;
+    const uint4 bk = __ldg(h.hot_buckets + bi);
+    const int j = bk.x == ka ? 0 : bk.y == ka ? 1 : bk.z == ka ? 2 : bk.w == ka ? 3 : -1;
+    if (j < 0) return !(bk.x && bk.y && bk.z && bk.w);  // not listed (its home bucket has room)
+    *out = __uint_as_float(__ldg(h.bucket_results + bi * 4 + j));  // listed: glibc's value
+    return true;
+}
+
+/// glibc expm1f / log1pf for any float (out of line and rare: arguments outside
+/// the LIF range and full buckets; tests/test_libm_parity.py sweeps every float).
+__device__ __noinline__ float glibc_exact(float x, bool is_log, const LibmTables* lt) {
+    return glibc_spec_resolved(x, is_log, *lt);
+}
+
+__device__ __forceinline__ float glibc_value(float x, bool is_log, const FusedProgram& p) {
+    float y;
+    return glibc_fast(x, is_log, p.libm, &y) ? y : glibc_exact(x, is_log, &p.libm);
+}
+
+/// Speculative glibc value (libm.cuh): the rounded polynomial, and whether it
+/// may differ from glibc's (then the lane's step is recomputed by a doubt batch).
+__device__ __forceinline__ float glibc_spec(float x, bool is_log, const FusedProgram& p, bool& doubtful) {
+    const LibmHash& h = p.libm.t[is_log ? 1 : 0];
+    const Spec sp = spec_any(x, is_log, h.region_w8, h.region_shift);
+    doubtful = doubtful || sp.doubtful;
+    return sp.r;
+}
+
+/// lif_spike_step<float> (neuron_math.hpp:55-77) of one lane from its step's
+/// v, r, J; F(x, is_log) evaluates expm1f / log1pf.  Returns whether it spiked.
+template <typename F>
+__device__ __forceinline__ bool lif_step(float J, float& v, float& r, float dt, float em_dt, double inv_tau_rc,
+                                         float tau_rc, float tau_ref, F&& f) {
     float delta = dt - r;
     if (delta < 0.0f) delta = 0.0f;
     if (delta > dt) delta = dt;
-    float vn = v - (J - v) * glibc_spec_resolved(-delta / tau_rc, false, t);
+    float em;
+    if (delta == dt) {
+        em = em_dt;  // expm1f(-dt / tau_rc): the host's glibc value
+    } else if (delta == 0.0f) {
+        em = -0.0f;  // expm1f(-0)
+    } else {
+        // == -delta / tau_rc in IEEE float: the double product is within 2^-52 of the quotient,
+        // and a quotient of floats is never within 2^-49 of a float midpoint unless on it,
+        // which needs a power-of-two divisor (then the product is exact)
+        em = f(static_cast<float>(static_cast<double>(-delta) * inv_tau_rc), false);
+    }
+    float vn = v - (J - v) * em;
     if (vn < 0.0f) vn = 0.0f;
     if (vn > 1.0f) {
-        const float since = -tau_rc * glibc_spec_resolved(-(vn - 1.0f) / (J - 1.0f), true, t);
+        const float since = -tau_rc * f(-(vn - 1.0f) / (J - 1.0f), true);
         v = 0.0f;
         r = tau_ref - since;
         return true;
@@ -346,115 +343,52 @@ __device__ __forceinline__ bool lif_exact(float J, float& v, float& r, float dt,
     return false;
 }
 
-/// Doubtful values (out of line: ~5% of the transcendentals).  The sweep
-/// stored the speculative v, r and spike bit.  A speculative value is glibc's
-/// unless its argument is table-listed, so the entry first re-derives the
-/// doubtful argument (cheap: the expm1 argument from r, the log1p argument
-/// from the refractory-free voltage) and asks the block filter; only a
-/// listed, out-of-range or compound case (a doubtful log1p after an exit)
-/// recomputes the step exactly and patches v, r and the spike bit.
-/// Lane l takes entry l of q[0, cnt).
-/// The exact step of one doubtful lane (out of line and rare: its code stays
-/// out of the sweep's instruction-cache footprint).
-__device__ __noinline__ void dq_exact(uint32_t key, float v, float r, float J, const FEns* e, float* A, int B, int b0,
-                                      uint32_t* words, const LibmTables* lt) {
-    const uint32_t i = key >> 5, col = key & 31u;
-    const int64_t o = static_cast<int64_t>(i) * B + b0 + col;
-    if (lif_exact(J, v, r, e->dt, e->tau_rc, e->tau_ref, *lt))
-        atomicOr(words + i, 1u << col);
-    else
-        atomicAnd(words + i, ~(1u << col));
-    A[e->v_base + o] = v;
-    A[e->r_base + o] = r;
+/// The exception queue's batch (lane l takes entry l of q[0, cnt)): the whole
+/// step of a neuron whose step needs a transcendental — it leaves the
+/// refractory period (0 < delta < dt, or NaN: expm1f) or it spikes (log1pf) —
+/// recomputed from its v, r, J with the speculative values.  v, r and the spike
+/// bit are written; a lane whose value was doubtful joins the doubt queue and
+/// is recomputed exactly by doubt_batch.  Returns the new doubt count.
+template <int BT>
+__device__ __forceinline__ int exc_batch(const FusedProgram& p, const FEns* ep, float* vcol, int64_t rdelta,
+                                         const QEnt* q, int cnt, QEnt* qd, int nd, uint32_t* words) {
+    const int lane = threadIdx.x & 31;
+    const bool on = lane < cnt;
+    const QEnt x = on ? q[lane] : QEnt{0u, 0.0f, 0.0f, 0.0f};  // idle lanes: delta = dt, no spike
+    float v = x.a, r = x.b;
+    bool doubtful = false;
+    const bool spike = lif_step(x.c, v, r, __ldg(&ep->dt), __ldg(&ep->em_dt), __ldg(&ep->inv_tau_rc),
+                                __ldg(&ep->tau_rc), __ldg(&ep->tau_ref),
+                                [&](float a, bool is_log) { return glibc_spec(a, is_log, p, doubtful); });
+    const uint32_t i = x.key >> 5, col = x.key & 31u;
+    if (on) {
+        float* vp = vcol + static_cast<int64_t>(i) * (BT > 0 ? BT : p.batch) + col;
+        vp[0] = v;
+        vp[rdelta] = r;
+        if (spike) atomicOr(words + i, 1u << col);  // exit lanes' bits are 0; spiking lanes' already set
+    }
+    const bool d = on && doubtful;
+    const uint32_t m = __ballot_sync(kFull, d);
+    if (d) qd[nd + __popc(m & lanemask_lt())] = x;
+    return nd + __popc(m);
 }
 
-/// Step constants of an ensemble the doubt resolution needs (passed in
-/// registers: re-reading them from the FEns in global memory put an L2 round
-/// trip in front of every batch).
-struct DqConst {
-    float dt, em_dt;
-    double inv_tau_rc;
-    const uint4* bk_e;  // bucketed LIF-range key sets of expm1 / log1p
-    const uint4* bk_l;
-    const uint32_t* br_e;  // their glibc results
-    const uint32_t* br_l;
-    float tau_rc, tau_ref;
-    float* vcol;     // v of row 0 of this tile's column 0 (A + v_base + b0)
-    int64_t rdelta;  // r_base - v_base
-    const uint8_t* w8e;  // the shared-memory screening tables (spec_any)
-    const uint8_t* w8l;
-    uint32_t w8_shift;
-    uint32_t bmask_e, bmask_l;
-    int bshift_e, bshift_l;
-    unsigned long long* prof;  // profile builds: counters (else null)
-};
-
-/// glibc's value of expm1f / log1pf (is_log) at x on the LIF range, without the
-/// slow paths: the rounded polynomial unless it is doubtful and x is listed in
-/// the bucketed table (then the table value).  Returns false when only the
-/// exact path can decide (x outside the LIF range, or a full bucket).
-__device__ __forceinline__ bool glibc_fast(float x, bool is_log, const DqConst& K, float* out) {
-    const Spec sp = spec_any(x, is_log, is_log ? K.w8l : K.w8e, K.w8_shift);
-    *out = sp.r;
-    if (!sp.doubtful) return true;
-    const uint32_t ka = __float_as_uint(x);
-    if (ka - 0x80000001u > 0x3D7FFFFFu) return false;  // outside the LIF range
-    const uint32_t bi = (ka * 0x9E3779B1u) >> (is_log ? K.bshift_l : K.bshift_e);
-    const uint4 bk = __ldg((is_log ? K.bk_l : K.bk_e) + bi);
-    const int j = bk.x == ka ? 0 : bk.y == ka ? 1 : bk.z == ka ? 2 : bk.w == ka ? 3 : -1;
-    if (j < 0) return !(bk.x && bk.y && bk.z && bk.w);  // not listed (its home bucket has room)
-    *out = __uint_as_float(__ldg((is_log ? K.br_l : K.br_e) + bi * 4 + j));  // listed: glibc's value
-    return true;
-}
-
-/// One batch of doubtful lanes (lane l takes entry l of q[0, cnt)): the step
-/// recomputed from the original v, r, J with glibc_fast for the transcendentals
-/// (the bucketed table instead of the exact path's probes); v, r and the spike
-/// bit are rewritten.  Only arguments outside the LIF range or full buckets
-/// fall through to dq_exact.
-__device__ __forceinline__ void dq_batch(const QEnt* q, int cnt, const DqConst& K, const FEns* e, float* A, int B,
-                                         int b0, uint32_t* words, const LibmTables* lt, int lane) {
+/// The doubt queue's batch: the step recomputed with glibc's exact values
+/// (bucketed table, else the exact path); v, r and the spike bit rewritten.
+template <int BT>
+__device__ __forceinline__ void doubt_batch(const FusedProgram& p, const FEns* ep, float* vcol, int64_t rdelta,
+                                            const QEnt* q, int cnt, uint32_t* words) {
+    const int lane = threadIdx.x & 31;
     if (lane >= cnt) return;
     const QEnt x = q[lane];
-    const uint32_t key = x.key & ~(kDoubtExp | kDoubtLog);
-    const float dt = K.dt, v0 = x.a, r0 = x.b, J = x.c;
-    // lif_spike_step<float> (neuron_math.hpp:55-77)
-    float delta = dt - r0;
-    if (delta < 0.0f) delta = 0.0f;
-    if (delta > dt) delta = dt;
-    bool ok = true;
-    float em;
-    if (delta == dt) {
-        em = K.em_dt;
-    } else if (delta == 0.0f) {
-        em = -0.0f;
-    } else {
-        const float xa = static_cast<float>(static_cast<double>(-delta) * K.inv_tau_rc);  // == -delta / tau_rc
-        ok = glibc_fast(xa, false, K, &em);
-    }
-    float vn = v0 - (J - v0) * em;
-    if (vn < 0.0f) vn = 0.0f;
-    const bool spike = vn > 1.0f;
-    float v = vn, r = r0 > dt ? r0 - dt : 0.0f;
-    if (ok && spike) {
-        float lg;
-        ok = glibc_fast(-(vn - 1.0f) / (J - 1.0f), true, K, &lg);
-        const float since = -K.tau_rc * lg;
-        v = 0.0f;
-        r = K.tau_ref - since;
-    }
-    if (K.prof) {  // profile builds: doubt entries, exact-path entries
-        atomicAdd(K.prof, 1ull);
-        if (!ok) atomicAdd(K.prof + 1, 1ull);
-    }
-    if (!ok) {
-        dq_exact(key, v0, r0, J, e, A, B, b0, words, lt);
-        return;
-    }
-    const uint32_t i = key >> 5, col = key & 31u;
-    float* vp = K.vcol + static_cast<int64_t>(i) * B + col;
+    float v = x.a, r = x.b;
+    const bool spike = lif_step(x.c, v, r, __ldg(&ep->dt), __ldg(&ep->em_dt), __ldg(&ep->inv_tau_rc),
+                                __ldg(&ep->tau_rc), __ldg(&ep->tau_ref),
+                                [&](float a, bool is_log) { return glibc_value(a, is_log, p); });
+    const uint32_t i = x.key >> 5, col = x.key & 31u;
+    float* vp = vcol + static_cast<int64_t>(i) * (BT > 0 ? BT : p.batch) + col;
     vp[0] = v;
-    vp[K.rdelta] = r;
+    vp[rdelta] = r;
     if (spike)
         atomicOr(words + i, 1u << col);
     else
@@ -673,7 +607,7 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
     const int b = b0 + lane;
     const bool valid = active && ((BT > 0 && BT % 32 == 0) || b < B);
     float* A = p.arena;
-    const LibmTables& lt = p.libm;
+    FTRACE(1, u);
 
     // stage encoders, biases and decoder products (async; overlaps the connection updates)
     if (threadIdx.x == 0) {
@@ -697,6 +631,7 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
     }
 
     // 1. connection updates of step k-1 (destination side) and the input sum, plan order
+    FTRACE(2, k);
     float* sin = S.in + tslot * DMAX * 32;
     if (active) {
         const int rper = (e.d + p.slices - 1) / p.slices;
@@ -737,50 +672,59 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
     float x[DMAX];
 #pragma unroll
     for (int j = 0; j < DMAX; ++j) x[j] = active ? sin[j * 32 + lane] : 0.0f;
+    __syncthreads();  // every warp holds its inputs in registers: the queues reuse `in`
+    FTRACE(4, 0);
     mbar_wait(S.bar, parity);
+    FTRACE(5, 0);
 
     // 2. neuron sweep over this warp's slice
     const int nper = ((e.n + p.slices - 1) / p.slices + 31) & ~31;
     const int n0 = min(e.n, slice * nper), n1 = min(e.n, n0 + nper);
     uint32_t* words = S.words + tslot * p.nmax;
-    QEnt* dq = S.dq + warp * kDQ;
-    int dn = 0;
     if (active && n0 < n1) {
-        const float dt = e.dt, em_dt = e.em_dt, tau_rc = e.tau_rc, tau_ref = e.tau_ref;
-        const double inv_tau_rc = e.inv_tau_rc;
+        const float dt = e.dt, em_dt = e.em_dt;
         const float2 dt2 = make_float2(dt, dt), ndt2 = make_float2(-dt, -dt);
         float* vrow0 = A + e.v_base + b0;  // row 0, column b0 of this tile
-        float* rrow0 = A + e.r_base + b0;
         float* ring = S.ring + warp * kRingFloats;
         const bool vec = (B & 3) == 0;
-        // L2 prefetch kL2Ahead rows ahead.  When the unit spans every column the
-        // rows are contiguous: lane 0 of the slice's first tile pulls 8 whole rows
-        // of v and of r with two bulk prefetches; otherwise lanes 0-15 pull their
-        // tile's 128-B segments of the 8 v and 8 r rows.
-        const bool pf_rows = p.groups == 1 && p.tu * 32 >= B && vec;
-        const bool pf_lane = pf_rows ? (tslot == 0 && lane == 0) : lane < 2 * kUnroll;
-        const float* pf_v = A + e.v_base + (pf_rows ? 0 : b0 + (lane & (kUnroll - 1)) * static_cast<int64_t>(B));
-        const float* pf_r = A + e.r_base + (pf_rows ? 0 : b0 + (lane & (kUnroll - 1)) * static_cast<int64_t>(B));
-        const float* pf_base = (pf_rows || lane < kUnroll) ? pf_v : pf_r;
         float* vst = vrow0 + static_cast<int64_t>(n0) * B + lane;  // row i of this lane
         const int64_t rdelta = e.r_base - e.v_base;
-        RingLane RL;
-        {
+        // the lane's share of the ring copies (addresses recomputed per round: fewer live
+        // registers).  vec (B % 4 == 0): 16 B, columns lc..lc+3 of row lr of each 4-row
+        // round; else 4 B (its own column) of every row
+        const uint32_t ring_s = smem_addr(ring);
+        auto ring_issue = [&](int st, int r0) {
             const int lr = vec ? (lane >> 3) : 0, lc = vec ? (lane & 7) * 4 : lane;
-            RL.src = vrow0 + static_cast<int64_t>(n0 + lr) * B + lc;
-            RL.rdelta = rdelta;
-            RL.dst = smem_addr(ring + lr * 32 + lc);
-            RL.row = lr;
-            RL.ok = b0 + lc < B;
-        }
-        ring_issue<BT>(RL, 0, n0, n0, n1, B, vec);
+            if (b0 + lc < B) {
+                const float* src = vrow0 + static_cast<int64_t>(r0 + lr) * B + lc;
+                const uint32_t dst = ring_s + (st * kUnroll * 32 + lr * 32 + lc) * 4;
+                if (vec) {
+                    if (r0 + lr < n1) {
+                        cp_async16_s(dst, src);
+                        cp_async16_s(dst + 2 * kUnroll * 32 * 4, src + rdelta);
+                    }
+                } else {
+#pragma unroll
+                    for (int rr = 0; rr < kUnroll; ++rr)
+                        if (r0 + rr < n1) {
+                            cp_async4_s(dst + rr * 32 * 4, src + static_cast<int64_t>(rr) * B);
+                            cp_async4_s(dst + rr * 32 * 4 + 2 * kUnroll * 32 * 4, src + static_cast<int64_t>(rr) * B + rdelta);
+                        }
+                }
+            }
+            cp_async_commit();
+        };
+        FTRACE(50, n0);
+        ring_issue(0, n0);
+        FTRACE(51, n1);
         const bool lv = (BT > 0 && BT % 32 == 0) ? true : valid;  // inside the sweep the tile is active
-        const DqConst dqk{dt, em_dt, inv_tau_rc, lt.t[0].hot_buckets, lt.t[1].hot_buckets, lt.t[0].bucket_results,
-                          lt.t[1].bucket_results, tau_rc, tau_ref, vrow0, rdelta, S.w8e, S.w8l, lt.t[0].region_shift,
-                          lt.t[0].bucket_mask,
-                          lt.t[1].bucket_mask, lt.t[0].bucket_shift, lt.t[1].bucket_shift,
-                          PROF ? p.prof + FS_COUNT : nullptr};
-        const uint32_t sh_e = lt.t[0].region_shift, sh_l = lt.t[1].region_shift;
+        const FEns* ep = p.ens + ei;
+        const uint32_t lt_mask = lanemask_lt();
+        // exception queues: the two branches of lif_spike_step that need a
+        // transcendental leave the sweep and are evaluated 32 lanes at a time
+        QEnt* qe = S.qe + warp * kQ;  // exceptions: leaving the refractory period (expm1f) or spiking (log1pf)
+        QEnt* qd = S.qs + warp * kQ;  // doubtful speculative values: recomputed exactly
+        int ne = 0, nd = 0;           // warp-uniform counts
         const float* ring_l = ring + lane;
         const float* sE = S.E + n0 * DMAX;
         const float* sbias = S.bias + n0;
@@ -789,17 +733,28 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
             if ((rel & (kUnroll - 1)) == 0) {
                 const int st = (rel / kUnroll) & 1;
                 __syncwarp();  // every lane's reads of the stage being refilled are done
-                ring_issue<BT>(RL, st ^ 1, i + kUnroll, n0, n1, B, vec);
+                FTRACE(52, i);
+                ring_issue(st ^ 1, i + kUnroll);
+                FTRACE(53, i);
                 cp_async_wait1();
                 __syncwarp();
+                FTRACE(54, i);
+                // L2 prefetch kL2Ahead rows ahead.  When the unit spans every column the
+                // rows are contiguous: lane 0 of the unit's first tile pulls kUnroll whole
+                // rows of v and of r with two bulk prefetches; otherwise lanes 0..2*kUnroll-1
+                // pull their tile's segments of the kUnroll v and r rows.
                 const int pi = i + kL2Ahead;
-                if (pf_lane && pi < n1) {
-                    if (pf_rows) {
-                        const uint32_t nb = static_cast<uint32_t>(min(kUnroll, n1 - pi) * B) * 4u;
-                        prefetch_l2_bulk(pf_v + static_cast<int64_t>(pi) * B, nb);
-                        prefetch_l2_bulk(pf_r + static_cast<int64_t>(pi) * B, nb);
-                    } else if (pi + (lane & (kUnroll - 1)) < n1) {
-                        const float* pa = pf_base + static_cast<int64_t>(pi) * B;
+                if (pi < n1) {
+                    if (p.groups == 1 && p.tu * 32 >= B && vec) {
+                        if (tslot == 0 && lane == 0) {
+                            const uint32_t nb = static_cast<uint32_t>(min(kUnroll, n1 - pi) * B) * 4u;
+                            const float* pv = vrow0 - b0 + static_cast<int64_t>(pi) * B;
+                            prefetch_l2_bulk(pv, nb);
+                            prefetch_l2_bulk(pv + rdelta, nb);
+                        }
+                    } else if (lane < 2 * kUnroll && pi + (lane & (kUnroll - 1)) < n1) {
+                        const float* pa = vrow0 + static_cast<int64_t>(pi + (lane & (kUnroll - 1))) * B +
+                                          (lane < kUnroll ? 0 : rdelta);
                         if (vec)
                             prefetch_l2_bulk(pa, static_cast<uint32_t>(min(32, B - b0)) * 4u);
                         else
@@ -808,6 +763,7 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
                 }
             }
             const float* sv = ring_l + (rel & (2 * kUnroll - 1)) * 32;
+            FTRACE(6, i);
             const float2 v2 = make_float2(sv[0], sv[32]);
             const float2 r2 = make_float2(sv[2 * kUnroll * 32], sv[2 * kUnroll * 32 + 32]);
             // DotInc(E, in, J) for neurons i, i+1: acc from +0, j ascending, then J = bias + acc.
@@ -834,76 +790,78 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
             const float2 J2 = __fadd2_rn(*reinterpret_cast<const float2*>(sbias), make_float2(acc[0], acc[1]));
             const float2 dl2 = __fadd2_rn(dt2, make_float2(-r2.x, -r2.y));  // dt - r
             const float2 rr2 = __fadd2_rn(r2, ndt2);                        // r - dt
-            // lif_spike_step<float> (neuron_math.hpp:55-77) with both transcendentals
-            // evaluated speculatively on every lane (at ~25% spikes and ~25% refractory
-            // exits per step nearly every warp row needs both): a double polynomial,
-            // rounded, exact unless `doubtful`; doubtful or out-of-range lanes are
-            // recomputed exactly in the doubt queue from their original v, r, J.
-            float em[2];
-            bool dbt[2];
+            // lif_spike_step<float> (neuron_math.hpp:55-77) for the lanes that need
+            // no transcendental: delta = dt (em = expm1f(-dt/tau_rc), the host's
+            // glibc value) or delta = 0 (em = expm1f(-0) = -0).  A lane with
+            // 0 < delta < dt (or NaN) goes to the exit queue; a spiking lane stores
+            // v = 0 and goes to the spike queue for its refractory time.
+            const float2 d2 = __fadd2_rn(J2, make_float2(-v2.x, -v2.y));  // J - v
+            bool ex[2];
+            float t[2];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const float delta = h ? dl2.y : dl2.x;  // clamp to [0, dt] below, NaN kept
+                const float delta = h ? dl2.y : dl2.x;
                 const bool ge = delta >= dt, le = delta <= 0.0f;
-                const bool ex = !ge && !le;  // 0 < delta < dt (or NaN): the step leaving the refractory period
-                // == -delta / tau_rc in IEEE float: the double product is within 2^-52 of the quotient,
-                // and a quotient of floats is never within 2^-49 of a float midpoint unless on it,
-                // which needs a power-of-two divisor (then the product is exact)
-                const float xa = static_cast<float>(static_cast<double>(-delta) * inv_tau_rc);
-                const Spec sa = spec_any(xa, false, S.w8e, sh_e);
-                em[h] = ex ? sa.r : (ge ? em_dt : -0.0f);  // expm1(-dt/tau_rc) from the host; expm1(-0) = -0
-                dbt[h] = ex && sa.doubtful;
+                ex[h] = !ge && !le;
+                t[h] = __fmul_rn(h ? d2.y : d2.x, ge ? em_dt : -0.0f);  // scalar products between paired sums
             }
-            // v - (J - v) * em: scalar products between the paired sums (see above)
-            const float2 d2 = __fadd2_rn(J2, make_float2(-v2.x, -v2.y));
-            const float t0 = __fmul_rn(d2.x, em[0]), t1 = __fmul_rn(d2.y, em[1]);
-            const float2 vn2 = __fadd2_rn(v2, make_float2(-t0, -t1));
+            const float2 vn2 = __fadd2_rn(v2, make_float2(-t[0], -t[1]));
             const bool two = i + 1 < n1;  // warp-uniform
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const bool row = lv && (h == 0 || two);
-                const float J = h ? J2.y : J2.x, vh = h ? v2.y : v2.x, rh = h ? r2.y : r2.x;
+                const float J = h ? J2.y : J2.x;
                 float vn = h ? vn2.y : vn2.x;
                 if (vn < 0.0f) vn = 0.0f;
-                const bool spike = vn > 1.0f;
-                const float xl = -(vn - 1.0f) / (J - 1.0f);
-                const Spec sl = spec_any(xl, true, S.w8l, sh_l);
-                const bool d = row && (dbt[h] || (spike && sl.doubtful));
-                const float since = -tau_rc * sl.r;
-                const float rn = spike ? tau_ref - since : (rh > dt ? (h ? rr2.y : rr2.x) : 0.0f);
-                if (row) {  // doubtful lanes too: their speculative values usually stand (see dq_batch)
+                const bool spike = !ex[h] && vn > 1.0f;
+                const float rh = h ? r2.y : r2.x;
+                if (row) {  // queued lanes store placeholders their batch overwrites
+#ifdef NENG_ROW_STORE_NORMAL
+                    vst[h * B] = spike ? 0.0f : vn;
+                    vst[h * B + rdelta] = rh > dt ? (h ? rr2.y : rr2.x) : 0.0f;
+#else
                     __stcs(vst + h * B, spike ? 0.0f : vn);
-                    __stcs(vst + h * B + rdelta, rn);
+                    __stcs(vst + h * B + rdelta, rh > dt ? (h ? rr2.y : rr2.x) : 0.0f);
+#endif
                 }
+                const uint32_t key = (static_cast<uint32_t>(i + h) << 5) | lane;
                 const uint32_t word = __ballot_sync(kFull, row && spike);
                 if (lane == 0 && (h == 0 || two)) words[i + h] = word;
-                const uint32_t dm = __ballot_sync(kFull, d);
-                if (dm) {  // warp-uniform
-                    if (d)
-                        dq[dn + __popc(dm & lanemask_lt())] =
-                            QEnt{(static_cast<uint32_t>(i + h) << 5) | lane | (dbt[h] ? kDoubtExp : 0u) |
-                                     (spike && sl.doubtful ? kDoubtLog : 0u),
-                                 vh, rh, J};
-                    dn += __popc(dm);
-                }
-                if (dn >= 32) {  // warp-uniform; a row adds <= 32, so dn < 32 before every row
-                    dn -= 32;
+                const bool xq = row && (ex[h] || spike);
+                const uint32_t me = __ballot_sync(kFull, xq);
+                if (xq) qe[ne + __popc(me & lt_mask)] = QEnt{key, h ? v2.y : v2.x, rh, J};
+                ne += __popc(me);
+                // warp-uniform drains; a row adds <= 32 entries, so ne < 32 before a row
+                if (ne >= 32) {
+                    ne -= 32;
                     __syncwarp();
                     tk.tick(FS_SWEEP);
-                    dq_batch(dq + dn, 32, dqk, p.ens + ei, A, B, b0, words, &p.libm, lane);
+                    FTRACE(9, ne);
+                    nd = exc_batch<BT>(p, ep, vrow0, rdelta, qe + ne, 32, qd, nd, words);
+                    FTRACE(10, nd);
+                    if (nd >= 32) {
+                        nd -= 32;
+                        __syncwarp();
+                        doubt_batch<BT>(p, ep, vrow0, rdelta, qd + nd, 32, words);
+                    }
                     __syncwarp();
                     tk.tick(FS_FIX);
                 }
             }
         }
-        if (dn > 0) {
+        __syncwarp();
+        FTRACE(11, ne);
+        if (ne > 0) nd = exc_batch<BT>(p, ep, vrow0, rdelta, qe, ne, qd, nd, words);
+        while (nd > 0) {  // <= 63 entries
             __syncwarp();
-            dq_batch(dq, dn, dqk, p.ens + ei, A, B, b0, words, &p.libm, lane);
-            __syncwarp();
-            dn = 0;
+            const int c = min(nd, 32);
+            nd -= c;
+            doubt_batch<BT>(p, ep, vrow0, rdelta, qd + nd, c, words);
         }
+        __syncwarp();
+        FTRACE(12, 0);
         // probes on the ensemble's own neuron signals (capture_probes, exec.cpp:328-338):
-        // read back after the doubt queue has patched v, r and the spike bits
+        // read back after the queues have written v, r and the spike bits
         for (int c = 0; c < e.sc_count; ++c) {
             const int2 cap = __ldg(reinterpret_cast<const int2*>(p.scaps) + e.sc_begin + c);
             float* dst = p.ring + p.ring_off[cap.y] + static_cast<int64_t>(k) * e.n * B + b;
@@ -964,6 +922,7 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
     }
 
     // 3. decode: rows [r0, r0 + R) of this warp's tile over all neurons, ascending
+    FTRACE(13, 0);
     if (active) {
         const int dx = e.dx;
         int R = (dx + p.slices - 1) / p.slices;
@@ -1030,6 +989,7 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
                 A[e.out_base + static_cast<int64_t>(i) * B + b] = (words[i] >> lane) & 1u ? e.amp_dt : 0.0f;
     }
     tk.tick(FS_DECODE);
+    FTRACE(14, 0);
     if (df_pos >= 0) {  // barrier-free schedule: destination-less connections, then publish the step
         __syncthreads();
         if (e.orph_count) {
@@ -1052,8 +1012,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fused_run_kernel(const _
         mbar_init(S.bar);
         mbar_init(S.bar2);
     }
-    for (uint32_t i = threadIdx.x; i < p.libm.t[0].n_regions; i += blockDim.x) S.w8e[i] = p.libm.t[0].region_w8[i];
-    for (uint32_t i = threadIdx.x; i < p.libm.t[1].n_regions; i += blockDim.x) S.w8l[i] = p.libm.t[1].region_w8[i];
     __syncthreads();
     uint32_t parity = 0;
     const int B = batch_of<BT>(p);

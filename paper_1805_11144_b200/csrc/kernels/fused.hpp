@@ -137,6 +137,9 @@ struct FusedProgram {
     int32_t n_free_orph = 0;
     const int32_t* dest_conns = nullptr;  // connections into an ensemble (the epilogue's)
     int32_t n_dest_conns = 0;
+    // fault localisation (builds with -DNENG_FUSED_TRACE, run with NENG_FUSED_TRACE=1): per warp
+    // (checkpoint, value) pairs in host-mapped memory, readable after the context has faulted
+    int32_t* trace = nullptr;
 };
 
 enum FusedSection { FS_DEFER, FS_IN, FS_SWEEP, FS_QUEUE, FS_FIX, FS_DECODE, FS_BAR, FS_EPI, FS_COUNT };

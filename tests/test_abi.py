@@ -58,6 +58,22 @@ def test_no_contracted_paired_fma_in_sass():
     assert not re.search(r"\bFFMA2\b", sass)
 
 
+def test_no_odd_uniform_memory_descriptors_in_sass():
+    """A 64-bit memory descriptor lives in an even/odd uniform register pair.
+    ptxas 12.9 emitted `LDGSTS ... desc[UR1]` for the cp.async with an
+    L2::cache_hint operand in some kernel instances, which faulted at run time
+    with "illegal instruction" (the round-1 "code-placement sensitive" fault).
+    The kernels no longer use that form; this keeps every descriptor even."""
+    import shutil
+    import subprocess
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", engine.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    odd = re.findall(r"^.*desc\[UR\d*[13579]\].*$", sass, flags=re.M)
+    assert not odd, odd[:4]
+
+
 def test_bad_arguments_fail_with_status_not_crash():
     lib = engine.lib()
     out = ctypes.c_void_p()

@@ -1,7 +1,6 @@
-# quick iteration on the GPU box: parity tests, then the bench (+ section profile)
+# iteration: fused parity tests + bench line (no CPU baseline) + short profile
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_fused.py tests/test_gpu_engine.py -x -q > gpurun_out/pytest_fused.log 2>&1; echo "pytest rc=$?"
-tail -30 gpurun_out/pytest_fused.log
-timeout 300 python bench.py --steps 300 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_iter.log 2>&1; echo "bench rc=$?"
-cat gpurun_out/bench_iter.log | tail -3
-NENG_FUSED_PROFILE=1 timeout 300 python bench.py --steps 100 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | grep -E "fused profile|error|Error" | tail -4
+timeout 900 python -m pytest tests/test_fused.py tests/test_baseline_sizes.py -m gpu -q -s -k "not config1" > gpurun_out/pytest_iter.log 2>&1; echo "pytest rc=$?"
+grep -E "passed|failed|FAILED|mismatch" gpurun_out/pytest_iter.log | tail -15
+timeout 300 python bench.py --steps 500 --warmup 5 --no-cpu-baseline > gpurun_out/bench_iter.log 2>&1; echo "bench rc=$?"
+tail -1 gpurun_out/bench_iter.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('ms/step', d['ms_per_step'], 'G', d['value']/1e9, 'frac', d['roofline']['frac'], 'e2e G', (d.get('e2e') or {}).get('value',0)/1e9)"
