@@ -51,7 +51,10 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kUnroll = 4;   // neuron rows per prefetch round (pairs inside)
 constexpr int kMinBlocks = 3;  // CTAs per SM the register budget is sized for
-constexpr int kL2Ahead = 24; // rows of v/r pulled into L2 ahead of the round being computed
+#ifndef NENG_L2_AHEAD
+#define NENG_L2_AHEAD 24
+#endif
+constexpr int kL2Ahead = NENG_L2_AHEAD;  // rows of v/r pulled into L2 ahead of the round being computed
 constexpr uint32_t kFull = 0xffffffffu;
 
 
@@ -684,19 +687,20 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
     if (active && n0 < n1) {
         const float dt = e.dt, em_dt = e.em_dt;
         const float2 dt2 = make_float2(dt, dt), ndt2 = make_float2(-dt, -dt);
-        float* vrow0 = A + e.v_base + b0;  // row 0, column b0 of this tile
+        // addresses inside the sweep derive from vst (row i, this lane's column): a
+        // separate row-0 pointer would be one more 64-bit value live across the loop
         float* ring = S.ring + warp * kRingFloats;
         const bool vec = (B & 3) == 0;
-        float* vst = vrow0 + static_cast<int64_t>(n0) * B + lane;  // row i of this lane
+        float* vst = A + e.v_base + b0 + static_cast<int64_t>(n0) * B + lane;  // row i of this lane
         const int64_t rdelta = e.r_base - e.v_base;
         // the lane's share of the ring copies (addresses recomputed per round: fewer live
         // registers).  vec (B % 4 == 0): 16 B, columns lc..lc+3 of row lr of each 4-row
         // round; else 4 B (its own column) of every row
         const uint32_t ring_s = smem_addr(ring);
-        auto ring_issue = [&](int st, int r0) {
+        auto ring_issue = [&](int st, int r0, const float* rowp) {  // rowp: row r0, this lane's column
             const int lr = vec ? (lane >> 3) : 0, lc = vec ? (lane & 7) * 4 : lane;
             if (b0 + lc < B) {
-                const float* src = vrow0 + static_cast<int64_t>(r0 + lr) * B + lc;
+                const float* src = rowp + static_cast<int64_t>(lr) * B + (lc - lane);
                 const uint32_t dst = ring_s + (st * kUnroll * 32 + lr * 32 + lc) * 4;
                 if (vec) {
                     if (r0 + lr < n1) {
@@ -715,7 +719,7 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
             cp_async_commit();
         };
         FTRACE(50, n0);
-        ring_issue(0, n0);
+        ring_issue(0, n0, vst);
         FTRACE(51, n1);
         const bool lv = (BT > 0 && BT % 32 == 0) ? true : valid;  // inside the sweep the tile is active
         const FEns* ep = p.ens + ei;
@@ -734,7 +738,7 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
                 const int st = (rel / kUnroll) & 1;
                 __syncwarp();  // every lane's reads of the stage being refilled are done
                 FTRACE(52, i);
-                ring_issue(st ^ 1, i + kUnroll);
+                ring_issue(st ^ 1, i + kUnroll, vst + kUnroll * B);
                 FTRACE(53, i);
                 cp_async_wait1();
                 __syncwarp();
@@ -746,14 +750,14 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
                 const int pi = i + kL2Ahead;
                 if (pi < n1) {
                     if (p.groups == 1 && p.tu * 32 >= B && vec) {
-                        if (tslot == 0 && lane == 0) {
+                        if (threadIdx.x == 0) {  // warp 0 owns tile slot 0
                             const uint32_t nb = static_cast<uint32_t>(min(kUnroll, n1 - pi) * B) * 4u;
-                            const float* pv = vrow0 - b0 + static_cast<int64_t>(pi) * B;
+                            const float* pv = vst + kL2Ahead * B;  // thread 0: tile 0, column 0
                             prefetch_l2_bulk(pv, nb);
                             prefetch_l2_bulk(pv + rdelta, nb);
                         }
                     } else if (lane < 2 * kUnroll && pi + (lane & (kUnroll - 1)) < n1) {
-                        const float* pa = vrow0 + static_cast<int64_t>(pi + (lane & (kUnroll - 1))) * B +
+                        const float* pa = vst - lane + static_cast<int64_t>(kL2Ahead + (lane & (kUnroll - 1))) * B +
                                           (lane < kUnroll ? 0 : rdelta);
                         if (vec)
                             prefetch_l2_bulk(pa, static_cast<uint32_t>(min(32, B - b0)) * 4u);
@@ -837,12 +841,13 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
                     __syncwarp();
                     tk.tick(FS_SWEEP);
                     FTRACE(9, ne);
-                    nd = exc_batch<BT>(p, ep, vrow0, rdelta, qe + ne, 32, qd, nd, words);
+                    float* vcol = vst - static_cast<int64_t>(i) * B - lane;  // row 0, column b0
+                    nd = exc_batch<BT>(p, ep, vcol, rdelta, qe + ne, 32, qd, nd, words);
                     FTRACE(10, nd);
                     if (nd >= 32) {
                         nd -= 32;
                         __syncwarp();
-                        doubt_batch<BT>(p, ep, vrow0, rdelta, qd + nd, 32, words);
+                        doubt_batch<BT>(p, ep, vcol, rdelta, qd + nd, 32, words);
                     }
                     __syncwarp();
                     tk.tick(FS_FIX);
@@ -851,6 +856,7 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
         }
         __syncwarp();
         FTRACE(11, ne);
+        float* vrow0 = A + __ldg(&ep->v_base) + b0;  // row 0, column b0 of this tile (reloaded: not live in the loop)
         if (ne > 0) nd = exc_batch<BT>(p, ep, vrow0, rdelta, qe, ne, qd, nd, words);
         while (nd > 0) {  // <= 63 entries
             __syncwarp();
