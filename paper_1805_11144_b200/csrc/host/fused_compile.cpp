@@ -563,12 +563,14 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
                 // up to even with a zero row (phase A takes neurons in pairs)
                 const Signal& Es = m.signals[e.E];
                 x.epad_off = align4();
+                // neuron pairs interleaved, [i / 2][j][i % 2]: the sweep sums two neurons side by side
                 const int n2 = (x.n + 1) & ~1;
-                for (int ii = 0; ii < n2; ++ii)
+                for (int i2 = 0; i2 < n2; i2 += 2)
                     for (int jj = 0; jj < DMAX; ++jj)
-                        values.push_back(ii < x.n && jj < x.d && !Es.initial.empty()
-                                             ? static_cast<float>(Es.initial[static_cast<size_t>(ii) * x.d + jj])
-                                             : 0.0f);
+                        for (int ii = i2; ii < i2 + 2; ++ii)
+                            values.push_back(ii < x.n && jj < x.d && !Es.initial.empty()
+                                                 ? static_cast<float>(Es.initial[static_cast<size_t>(ii) * x.d + jj])
+                                                 : 0.0f);
             }
             x.in_init_off = push_values(m.operators[e.rin].value);
             x.xhat_init_off = push_values(m.operators[e.rx].value);

@@ -121,6 +121,38 @@ __device__ __forceinline__ void prefetch_l2_line(const void* p) {
     } while (0)
 #endif
 
+// Paired fp32 arithmetic.  ptxas contracts mul.rn.f32x2 feeding add.rn.f32x2
+// into FFMA2 (one rounding) even under -fmad=false, so a paired product is
+// formed as fma(a, b, -0) — exactly the rounded product (x + -0 == x for every
+// x, -0 included) — with the -0 pair from the kernel parameters, which ptxas
+// cannot fold away (tests/test_abi.py checks every FFMA2's addend in the SASS).
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float2 unpk2(uint64_t v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ uint64_t mul2_exact(uint64_t a, uint64_t b, uint64_t neg_zero2) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(neg_zero2));
+    return r;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+/// Encoder element (i, j) in the pair-interleaved layout [i / 2][DMAX][2].
+template <int DMAX>
+__device__ __forceinline__ float enc_at(const float* E, int i, int j) {
+    return E[(i >> 1) * 2 * DMAX + j * 2 + (i & 1)];
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -770,26 +802,21 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
             FTRACE(6, i);
             const float2 v2 = make_float2(sv[0], sv[32]);
             const float2 r2 = make_float2(sv[2 * kUnroll * 32], sv[2 * kUnroll * 32 + 32]);
-            // DotInc(E, in, J) for neurons i, i+1: acc from +0, j ascending, then J = bias + acc.
-            // Products two dims at a time (FMUL2), sums scalar and in order.  A
-            // paired product must never feed a paired sum: ptxas contracts
-            // FMUL2 -> FADD2 into FFMA2 even for .rn (tests/test_abi.py checks the SASS).
+            // DotInc(E, in, J) for neurons i, i+1: acc from +0, j ascending, then J = bias + acc;
+            // the two neurons' sums side by side (encoders pair-interleaved: [j][i, i+1])
             float acc[2];
+            {
+                const float4* er = reinterpret_cast<const float4*>(sE);
+                uint64_t a2 = 0;  // (+0, +0)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const float4* er = reinterpret_cast<const float4*>(sE + h * DMAX);
-                float a = 0.0f;
-#pragma unroll
-                for (int q = 0; q < DMAX / 4; ++q) {
+                for (int q = 0; q < DMAX / 2; ++q) {
                     const float4 w = er[q];
-                    const float2 m0 = __fmul2_rn(make_float2(w.x, w.y), make_float2(x[4 * q], x[4 * q + 1]));
-                    const float2 m1 = __fmul2_rn(make_float2(w.z, w.w), make_float2(x[4 * q + 2], x[4 * q + 3]));
-                    a = a + m0.x;
-                    a = a + m0.y;
-                    a = a + m1.x;
-                    a = a + m1.y;
+                    a2 = add2(a2, mul2_exact(pk2(w.x, w.y), pk2(x[2 * q], x[2 * q]), p.neg_zero2));
+                    a2 = add2(a2, mul2_exact(pk2(w.z, w.w), pk2(x[2 * q + 1], x[2 * q + 1]), p.neg_zero2));
                 }
-                acc[h] = a;
+                const float2 a = unpk2(a2);
+                acc[0] = a.x;
+                acc[1] = a.y;
             }
             const float2 J2 = __fadd2_rn(*reinterpret_cast<const float2*>(sbias), make_float2(acc[0], acc[1]));
             const float2 dl2 = __fadd2_rn(dt2, make_float2(-r2.x, -r2.y));  // dt - r
@@ -878,16 +905,9 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
                 } else if (cap.x == SC_VOLTAGE || cap.x == SC_REFRACTORY) {
                     val = vrow0[static_cast<int64_t>(i) * B + lane + (cap.x == SC_REFRACTORY ? rdelta : 0)];
                 } else {
-                    const float4* er = reinterpret_cast<const float4*>(S.E + i * DMAX);
                     float a = 0.0f;
 #pragma unroll
-                    for (int q = 0; q < DMAX / 4; ++q) {
-                        const float4 w = er[q];
-                        a = a + w.x * x[4 * q];
-                        a = a + w.y * x[4 * q + 1];
-                        a = a + w.z * x[4 * q + 2];
-                        a = a + w.w * x[4 * q + 3];
-                    }
+                    for (int j = 0; j < DMAX; ++j) a = a + enc_at<DMAX>(S.E, i, j) * x[j];
                     val = S.bias[i] + a;
                 }
                 dst[static_cast<int64_t>(i) * B] = val;
@@ -896,16 +916,9 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
         // the call's last step leaves J in the arena (DotInc(E, in, J) as above, once)
         if (last && valid) {
             for (int i = n0; i < n1; ++i) {
-                const float4* er = reinterpret_cast<const float4*>(S.E + i * DMAX);
                 float a = 0.0f;
 #pragma unroll
-                for (int q = 0; q < DMAX / 4; ++q) {
-                    const float4 w = er[q];
-                    a = a + w.x * x[4 * q];
-                    a = a + w.y * x[4 * q + 1];
-                    a = a + w.z * x[4 * q + 2];
-                    a = a + w.w * x[4 * q + 3];
-                }
+                for (int j = 0; j < DMAX; ++j) a = a + enc_at<DMAX>(S.E, i, j) * x[j];
                 A[e.j_base + static_cast<int64_t>(i) * B + b] = S.bias[i] + a;
             }
         }

@@ -41,7 +41,7 @@ struct FEns {
     int32_t in_init_off, xhat_init_off;                            // Reset payloads in `values`
     int32_t xb_row;          // first row of this ensemble's xhat in the parity buffers
     int64_t bias_off;        // Reset(J) payload, n_pad floats (16-B aligned)
-    int64_t epad_off;        // encoders [n (even)][DMAX], rows zero padded (16-B aligned)
+    int64_t epad_off;        // encoders [n (even) / 2][DMAX][2] (neuron pairs interleaved), rows zero padded (16-B aligned)
     int64_t dec_scaled_off;  // fp32(D[r,i]) * fp32(amp/dt), transposed [n][dx] — the DotInc term of a spike
     int32_t dec_bytes;       // n*dx*4 rounded up to 16 (bulk-copy size)
     float dt, tau_rc, tau_ref, amplitude;
@@ -107,6 +107,7 @@ struct FusedProgram {
     int32_t pmax_floats = 0;  // max over ensembles of n*dx rounded up to 4
     int64_t step_base = 0, time_base = 0;
     float dt = 0.f;
+    uint64_t neg_zero2 = 0x8000000080000000ull;  // (-0, -0): the addend of an exact paired product (fused.cu)
     LibmTables libm;
     // per call
     const float* feed_data = nullptr;
