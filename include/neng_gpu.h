@@ -164,14 +164,16 @@ typedef struct neng_device_cfg {
      * parity buffer between per-step calls (neng_gpu_call_*). */
     int32_t shard_rank, shard_count;
     /* NENG_PRECISION_*: STRICT_FP32 (default) reproduces EngineCore<float> bit for
-     * bit; TF32 runs dense DotInc groups (shared 2-D weights >= 32x32, per-batch
-     * input and output, batch >= 32) as tensor-core GEMMs with fp32 accumulation
-     * (TF32 products: a stated tolerance instead of bit-exact results). */
+     * bit; TF32 and BF16X3 run dense DotInc groups (shared 2-D weights with K >= 32,
+     * per-batch input and output, batch >= 32, 16-byte aligned rows) on the
+     * tcgen05 tensor cores with fp32 accumulation in TMEM: TF32 products (10-bit
+     * mantissa), or BF16X3 (each operand split into bf16 hi + lo, three MMAs:
+     * ~16-bit products) — a stated tolerance instead of bit-exact results. */
     int32_t precision;
     int32_t reserved[2];
 } neng_device_cfg;
 
-enum { NENG_PRECISION_STRICT_FP32 = 0, NENG_PRECISION_TF32 = 1 };
+enum { NENG_PRECISION_STRICT_FP32 = 0, NENG_PRECISION_TF32 = 1, NENG_PRECISION_BF16X3 = 2 };
 
 typedef struct neng_engine neng_engine;
 
@@ -259,6 +261,16 @@ int64_t neng_gpu_last_launch_count(const neng_engine* e);
 #define NENG_SCHED_FUSED_STEPPED 2
 #define NENG_SCHED_FUSED_BARRIER_FREE 4
 int32_t neng_gpu_last_schedule(const neng_engine* e);
+
+/* The tensor-core DotInc of the TF32 / BF16X3 precision modes on its own
+ * (tc_dot.cu), for tests and measurement:  Y[m][n] += A[m][k] X[k][n] with
+ * row-major host arrays (n, k multiples of 4; BF16X3: n, k multiples of 8).
+ * mode: NENG_PRECISION_TF32 or NENG_PRECISION_BF16X3.  y receives the result
+ * of one launch; *ms_out (may be NULL) = the mean device time of a launch over
+ * `reps` further back-to-back launches (CUDA events), the split of X included
+ * for BF16X3. */
+neng_status neng_gpu_tc_dot(int32_t mode, int32_t m, int32_t k, int32_t n, const float* a, const float* x,
+                            float* y, int32_t reps, double* ms_out);
 
 /* Error text of the engine's last failing call ("" if none). */
 const char* neng_gpu_last_error(const neng_engine* e);

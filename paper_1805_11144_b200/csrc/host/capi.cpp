@@ -191,6 +191,50 @@ neng_status neng_gpu_probe_info(const neng_engine* e, int32_t i, int32_t* key, i
     return NENG_OK;
 }
 
+neng_status neng_gpu_tc_dot(int32_t mode, int32_t m, int32_t k, int32_t n, const float* a, const float* x,
+                            float* y, int32_t reps, double* ms_out) {
+    return guarded(nullptr, [&] {
+        if (!a || !x || !y || m < 1 || k < 1 || n < 1 || reps < 1)
+            throw nengb::InvalidArgument("neng_gpu_tc_dot: bad argument");
+        if (mode != NENG_PRECISION_TF32 && mode != NENG_PRECISION_BF16X3)
+            throw nengb::InvalidArgument("neng_gpu_tc_dot: mode must be TF32 or BF16X3");
+        const int tm = mode == NENG_PRECISION_TF32 ? nengb::TC_TF32 : nengb::TC_BF16X3;
+        auto check = [](cudaError_t e, const char* what) { nengb::cuda_check(e, what); };
+        const size_t ab = size_t(m) * k * 4, xb = size_t(k) * n * 4, yb = size_t(m) * n * 4;
+        nengb::DevMem da, dx, dy, dy0, scr;
+        da.ensure(ab);
+        dx.ensure(xb);
+        dy.ensure(yb);
+        dy0.ensure(yb);
+        if (tm == nengb::TC_BF16X3) scr.ensure(nengb::tc_dot_scratch_bytes(m, k, n));
+        check(cudaMemcpy(da.p, a, ab, cudaMemcpyHostToDevice), "tc_dot H2D");
+        check(cudaMemcpy(dx.p, x, xb, cudaMemcpyHostToDevice), "tc_dot H2D");
+        check(cudaMemcpy(dy0.p, y, yb, cudaMemcpyHostToDevice), "tc_dot H2D");
+        nengb::TcDotDesc d;
+        const char* why = nengb::tc_dot_prepare(&d, da.as<float>(), dx.as<float>(), dy.as<float>(), m, k, n, n, n, tm,
+                                                scr.p);
+        if (*why) throw nengb::InvalidArgument(std::string("neng_gpu_tc_dot: ") + why);
+        check(nengb::tc_dot_split_a(d, nullptr), "tc_dot split");
+        cudaEvent_t e0, e1;
+        check(cudaEventCreate(&e0), "event");
+        check(cudaEventCreate(&e1), "event");
+        // the result: one launch on the caller's Y
+        check(cudaMemcpy(dy.p, dy0.p, yb, cudaMemcpyDeviceToDevice), "tc_dot restore");
+        check(nengb::tc_dot_launch(d, nullptr), "tc_dot launch");
+        check(cudaMemcpy(y, dy.p, yb, cudaMemcpyDeviceToHost), "tc_dot D2H");
+        // the time: `reps` launches back to back (Y accumulates; its values are not returned)
+        check(cudaEventRecord(e0, nullptr), "event");
+        for (int r = 0; r < reps; ++r) check(nengb::tc_dot_launch(d, nullptr), "tc_dot launch");
+        check(cudaEventRecord(e1, nullptr), "event");
+        check(cudaEventSynchronize(e1), "tc_dot run");
+        float ms = 0.0f;
+        check(cudaEventElapsedTime(&ms, e0, e1), "event");
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (ms_out) *ms_out = ms / reps;
+    });
+}
+
 const char* neng_gpu_last_error(const neng_engine* e) { return e ? e->impl.last_error.c_str() : ""; }
 const char* neng_last_error(void) { return g_last_error.c_str(); }
 

@@ -16,8 +16,6 @@
 #include <thread>
 #include <unordered_map>
 
-#include <cublas_v2.h>
-
 #include "fused.hpp"
 
 namespace nengb {
@@ -324,7 +322,8 @@ Engine::Engine(PlannedModel planned, int batch, int unroll, const neng_device_cf
         shard_count_ = cfg->shard_count > 0 ? cfg->shard_count : 1;
         precision_ = cfg->precision;
     }
-    if (precision_ != NENG_PRECISION_STRICT_FP32 && precision_ != NENG_PRECISION_TF32)
+    if (precision_ != NENG_PRECISION_STRICT_FP32 && precision_ != NENG_PRECISION_TF32 &&
+        precision_ != NENG_PRECISION_BF16X3)
         throw BuildError("unknown precision mode " + std::to_string(precision_));
     if (shard_count_ < 1 || shard_rank_ < 0 || shard_rank_ >= shard_count_)
         throw BuildError("shard rank " + std::to_string(shard_rank_) + " is outside [0, " +
@@ -338,7 +337,6 @@ Engine::Engine(PlannedModel planned, int batch, int unroll, const neng_device_cf
 
 Engine::~Engine() {
     fused_.reset();
-    if (cublas_) cublasDestroy(static_cast<cublasHandle_t>(cublas_));
     for (cudaEvent_t& ev : feed_events_)
         if (ev) cudaEventDestroy(ev);
     for (cudaEvent_t& ev : xpose_events_)
@@ -450,6 +448,7 @@ void Engine::compile_generic() {
     std::vector<DTile> tiles;
     std::vector<float> values;
     int max_tiles = 1;
+    std::vector<char> written_sig;  // lazily: signals some operator writes
     for (const OpGroup& og : pm_.plan) {
         if (og.members.empty()) throw BuildError("plan has an empty group");
         auto fit = by_id.find(og.members[0]);
@@ -574,19 +573,46 @@ void Engine::compile_generic() {
                 g.flags |= GF_DENSE;
             }
         }
-        if (precision_ == NENG_PRECISION_TF32 && first.kind == OpKind::DotInc && batch_ >= 32 &&
+        if (precision_ != NENG_PRECISION_STRICT_FP32 && first.kind == OpKind::DotInc && batch_ >= 32 &&
             (g.flags & GF_PER_BATCH) && !(g.flags & (GF_SERIAL_ALL | GF_SERIAL_B))) {
-            // C[M][B] += A[M][K] X[K][B]: shared row-major weights, per-batch input and output
+            // Y[M][B] += A[M][K] X[K][B]: shared row-major weights, per-batch input and output,
+            // every member on the tensor cores or the whole group stays in the interpreter
             TcGroup tg;
             tg.group = static_cast<int>(groups.size());
+            const int mode = precision_ == NENG_PRECISION_TF32 ? TC_TF32 : TC_BF16X3;
+            float* Ab = arena_.as<float>();
+            if (written_sig.empty()) {  // signals some operator writes (BF16X3 splits A once per call)
+                written_sig.assign(m.signals.size(), 0);
+                for (const Operator& o : m.operators)
+                    for (int wp : written_positions(o)) written_sig[o.operands[wp].signal] = 1;
+            }
             bool ok = true;
             for (int mi = g.member_begin; mi < static_cast<int>(members.size()) && ok; ++mi) {
+                const Operator& mop = *by_id.at(og.members[mi - g.member_begin]);
+                if (mode == TC_BF16X3 && written_sig[mop.operands[0].signal]) {
+                    ok = false;
+                    break;
+                }
                 const DMember& dm = members[mi];
                 const DArg &A = dm.a[0], &X = dm.a[1], &Y = dm.a[2];
                 const int64_t M = Y.elems, K = X.elems;
                 ok = A.bs == 0 && A.es == 1 && A.elems == M * K && X.es == batch_ && X.bs == 1 && Y.es == batch_ &&
-                     Y.bs == 1 && M >= 1 && K >= 32;
-                if (ok) tg.gemms.push_back({A.base, X.base, Y.base, static_cast<int>(M), static_cast<int>(K)});
+                     Y.bs == 1 && M >= 1 && K >= 32 && M < (1 << 30) && K < (1 << 30);
+                // the output rows must not overlap the operands (they are read by TMA while it is written)
+                ok = ok && (Y.base + M * batch_ <= X.base || X.base + K * batch_ <= Y.base) &&
+                     (Y.base + M * batch_ <= A.base || A.base + M * K <= Y.base);
+                if (!ok) break;
+                void* scr = nullptr;
+                if (mode == TC_BF16X3) {
+                    tg.scratch.push_back(std::make_unique<DevMem>());
+                    tg.scratch.back()->ensure(tc_dot_scratch_bytes(static_cast<int>(M), static_cast<int>(K), batch_));
+                    scr = tg.scratch.back()->p;
+                }
+                TcDotDesc d;
+                const char* why = tc_dot_prepare(&d, Ab + A.base, Ab + X.base, Ab + Y.base, static_cast<int>(M),
+                                                 static_cast<int>(K), batch_, batch_, batch_, mode, scr);
+                ok = *why == 0;
+                if (ok) tg.dots.push_back(d);
             }
             if (ok) tc_groups_.push_back(std::move(tg));
         }
@@ -729,6 +755,13 @@ void Engine::launch_steps(int n_steps, const float* d_feed_data, const std::vect
     p.ring = d_ring;
     p.call_steps = n_steps;
     if (!tc_groups_.empty()) {
+        // BF16X3: the weights' bf16 halves, once per call (a DotInc's weights are shared and
+        // constant inside a call: no operator of a dense group writes its own A)
+        for (const TcGroup& tg : tc_groups_)
+            for (const TcDotDesc& d : tg.dots) {
+                cuda_check(tc_dot_split_a(d, stream), "tensor-core weight split");
+                if (d.mode == TC_BF16X3) ++last_launches_;
+            }
         // per step: interpreter segments between the tensor-core groups (feeds with the
         // first segment, probe captures with the last), the GEMMs in stream order between
         for (int k = 0; k < n_steps; ++k) {
@@ -741,8 +774,8 @@ void Engine::launch_steps(int n_steps, const float* d_feed_data, const std::vect
                     cuda_check(launch_generic(q, grid_, k, k + 1, 0, stream), "generic kernel launch");
                     ++last_launches_;
                 }
-                run_tc_gemms(tg, stream);
-                last_launches_ += static_cast<int64_t>(tg.gemms.size());
+                run_tc_dots(tg, stream);
+                last_launches_ += static_cast<int64_t>(tg.dots.size()) * (precision_ == NENG_PRECISION_BF16X3 ? 2 : 1);
                 seg = tg.group + 1;
             }
             GenericProgram q = p;
@@ -762,23 +795,8 @@ void Engine::launch_steps(int n_steps, const float* d_feed_data, const std::vect
     cuda_check(cudaStreamSynchronize(stream), "generic run");
 }
 
-void Engine::run_tc_gemms(const TcGroup& tg, cudaStream_t stream) {
-    if (!cublas_) {
-        cublasHandle_t h = nullptr;
-        if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasCreate failed");
-        cublas_ = h;
-    }
-    cublasHandle_t h = static_cast<cublasHandle_t>(cublas_);
-    if (cublasSetStream(h, stream) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream failed");
-    const float one = 1.0f;
-    float* A = arena_.as<float>();
-    for (const TcGemm& g : tg.gemms) {
-        // row-major C[M][B] += A[M][K] X[K][B]  ==  column-major C^T (B x M) += X^T (B x K) A^T (K x M)
-        cublasStatus_t st = cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, batch_, g.m, g.k, &one, A + g.x, CUDA_R_32F,
-                                         batch_, A + g.a, CUDA_R_32F, g.k, &one, A + g.y, CUDA_R_32F, batch_,
-                                         CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT);
-        if (st != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasGemmEx failed: " + std::to_string(static_cast<int>(st)));
-    }
+void Engine::run_tc_dots(const TcGroup& tg, cudaStream_t stream) {
+    for (const TcDotDesc& d : tg.dots) cuda_check(tc_dot_launch(d, stream), "tensor-core DotInc launch");
 }
 
 void Engine::run(int n_steps, int n_feeds, const neng_feed* feeds, double* probes_out) {

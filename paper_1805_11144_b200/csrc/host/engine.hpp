@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../kernels/program.hpp"
+#include "../kernels/tc_dot.hpp"
 #include "host_ir.hpp"
 
 namespace nengb {
@@ -124,18 +125,14 @@ class Engine {
     int device_ = 0, mode_ = NENG_MODE_GENERIC, requested_mode_ = NENG_MODE_AUTO, steps_per_launch_ = 0;
     int shard_rank_ = 0, shard_count_ = 1;
     int precision_ = NENG_PRECISION_STRICT_FP32;
-    // dense DotInc groups run as tensor-core GEMMs (precision_ == TF32)
-    struct TcGemm {
-        int64_t a, x, y;  // arena offsets: A [M][K] shared, X [K][B], Y [M][B]
-        int m, k;
-    };
+    // dense DotInc groups run on the tcgen05 tensor cores (precision_ TF32 / BF16X3, tc_dot.cu)
     struct TcGroup {
         int group;
-        std::vector<TcGemm> gemms;
+        std::vector<TcDotDesc> dots;  // one per member: Y[M][B] += A[M][K] X[K][B]
+        std::vector<std::unique_ptr<DevMem>> scratch;  // BF16X3 split buffers
     };
     std::vector<TcGroup> tc_groups_;
-    void* cublas_ = nullptr;  // cublasHandle_t
-    void run_tc_gemms(const TcGroup& g, cudaStream_t stream);
+    void run_tc_dots(const TcGroup& g, cudaStream_t stream);
     int call_steps_ = 0;  // steps of the open stepped call (0: none)
     cudaStream_t call_stream_ = nullptr;
     cudaStream_t stream_ = nullptr;

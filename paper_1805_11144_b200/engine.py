@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libneng_gpu.so")
 
 MODE_AUTO, MODE_GENERIC, MODE_FUSED = 0, 1, 2
-PRECISION_STRICT_FP32, PRECISION_TF32 = 0, 1
+PRECISION_STRICT_FP32, PRECISION_TF32, PRECISION_BF16X3 = 0, 1, 2
 STEP_FIRST_UPDATE, STEP_EPILOGUE = 1, 2
 SCHED_GENERIC, SCHED_FUSED_STEPPED, SCHED_BARRIER_FREE = 1, 2, 4  # neng_gpu_last_schedule bits
 
@@ -65,6 +65,9 @@ def lib():
         L.neng_gpu_last_error.argtypes = [P]
         L.neng_gpu_last_error.restype = C.c_char_p
         L.neng_last_error.restype = C.c_char_p
+        f32p = C.POINTER(C.c_float)
+        L.neng_gpu_tc_dot.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, f32p, f32p, f32p, C.c_int32,
+                                      C.POINTER(C.c_double)]
         _lib = L
     return _lib
 
@@ -205,3 +208,23 @@ class GpuEngine:
     def last_schedule(self) -> int:
         """NENG_SCHED_* bits of the most recent call (SCHED_BARRIER_FREE: the bench's kernel)."""
         return lib().neng_gpu_last_schedule(self._h)
+
+
+def tc_dot(a, x, y, precision: int = PRECISION_TF32, reps: int = 1):
+    """Y + A.X on the tcgen05 tensor-core DotInc (the TF32 / BF16X3 path of dense
+    DotInc groups) for host float32 arrays A [m][k], X [k][n], Y [m][n].
+    Returns (result, mean ms per launch)."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.array(y, dtype=np.float32, order="C", copy=True)
+    m, k = a.shape
+    k2, n = x.shape
+    if k2 != k or out.shape != (m, n):
+        raise ValueError("tc_dot: shape mismatch")
+    ms = C.c_double(0.0)
+    f32p = C.POINTER(C.c_float)
+    st = lib().neng_gpu_tc_dot(precision, m, k, n, a.ctypes.data_as(f32p), x.ctypes.data_as(f32p),
+                               out.ctypes.data_as(f32p), reps, C.byref(ms))
+    if st != 0:
+        raise RuntimeError(lib().neng_last_error().decode())
+    return out, ms.value

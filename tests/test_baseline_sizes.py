@@ -171,3 +171,37 @@ def test_config1_full_size_1000_steps():
     for s in pm.model.signals[::37]:
         for b in (0, w.batch - 1):
             assert np.array_equal(gpu.read_signal(s.id, b).view(np.uint64), ref.read_signal(s.id, b).view(np.uint64))
+
+
+def test_config3_tensor_core_paths_full_batch():
+    # Config 3 at B=512, 100 steps: the dense DotInc layers on the tcgen05 tensor
+    # cores (TF32, BF16X3) against the strict fp32 path (itself bit-exact with the
+    # reference, test_config3_strict_full_batch).  Stated tolerances:
+    #   rate-coded output (per-sample mean of the filtered output over the second
+    #   half of the run): relative L2 <= 10% (TF32), <= 1% (BF16X3);
+    #   hidden-layer spike counts over the run: fraction of (sample, neuron) counts
+    #   that differ <= 25% (TF32), <= 2% (BF16X3) — near-threshold neurons flip under
+    #   the products' rounding and the difference feeds back through the spikes.
+    from paper_1805_11144_b200.engine import PRECISION_BF16X3, PRECISION_TF32
+    steps = 100
+    w = networks.config3(steps=steps)
+    m = w.model
+    spike_keys = add_probes(m, [(_ens_signal(m, "l1.out"), "l1.spikes"), (_ens_signal(m, "l2.out"), "l2.spikes")])
+    pm = passes.run_passes(m)
+    strict = GpuEngine(pm, w.batch).run(steps, w.feeds)
+    (out_key,) = [k for k in strict if k not in spike_keys]
+    ref_rate = strict[out_key][:, steps // 2:].mean(axis=1)
+    assert np.abs(ref_rate).max() > 0.1  # the network is active
+    limits = {PRECISION_TF32: (0.10, 0.25), PRECISION_BF16X3: (0.01, 0.02)}
+    for prec, (rate_tol, spike_tol) in limits.items():
+        eng = GpuEngine(pm, w.batch, precision=prec)
+        got = eng.run(steps, w.feeds)
+        assert eng.last_launch_count() > steps  # the dense layers left the interpreter
+        rate = got[out_key][:, steps // 2:].mean(axis=1)
+        rel = float(np.linalg.norm(rate - ref_rate) / np.linalg.norm(ref_rate))
+        inst = float(np.linalg.norm(got[out_key] - strict[out_key]) / np.linalg.norm(strict[out_key]))
+        mism = [spike_count_mismatch(got[k], strict[k]) for k in spike_keys]
+        print(f"\nconfig3 B=512 {'TF32' if prec == PRECISION_TF32 else 'BF16X3'}: rate rel L2 {rel:.2e}, "
+              f"filtered-output rel L2 {inst:.2e}, spike-count mismatch l1 {mism[0]:.2e} l2 {mism[1]:.2e}")
+        assert rel <= rate_tol
+        assert max(mism) <= spike_tol

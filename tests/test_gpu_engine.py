@@ -248,9 +248,9 @@ def test_committed_golden_fixtures(name):
 
 def test_config3_strict_matches_reference_and_tf32_within_tolerance():
     # BASELINE config 3 (spiking MLP 784-1024-1024-10), batch and steps reduced for the CPU reference.
-    # Strict fp32 is bit-exact; the TF32 tensor-core path (dense DotInc as cuBLAS TF32 GEMMs with fp32
-    # accumulation) is held to the stated tolerance: the rate-coded output (mean of the filtered output
-    # over the second half of the run, per sample) within 10% relative L2 of the strict result.
+    # Strict fp32 is bit-exact; the TF32 tensor-core path (dense DotInc on tcgen05 with fp32 accumulation
+    # in TMEM, tc_dot.cu) is held to the stated tolerance: the rate-coded output (mean of the filtered
+    # output over the second half of the run, per sample) within 10% relative L2 of the strict result.
     from paper_1805_11144_b200.engine import PRECISION_TF32
     w = networks.config3(steps=40, batch=32)
     pm = passes.run_passes(w.model)
