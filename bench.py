@@ -52,6 +52,10 @@ def parse():
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
                     help="--shard batch: 'strong' splits the global minibatch (--batch) into batch/N rows per GPU; "
                          "'weak' runs --batch rows on every GPU")
+    ap.add_argument("--config", type=int, choices=[0, 1, 2, 3, 4], default=4,
+                    help="BASELINE.json configuration (4 = the headline 1M-neuron network; 0-3 run on rank 0 only)")
+    ap.add_argument("--precision", choices=["fp32", "tf32", "bf16x3"], default="fp32",
+                    help="dense DotInc groups (config 3): strict fp32 (bit-exact) or the tcgen05 tensor cores")
     ap.add_argument("--shard", choices=["batch", "ensemble"], default="batch",
                     help="multi-GPU mode: 'batch' = one minibatch replica per GPU (weak scaling, no collective); "
                          "'ensemble' = the ensembles split across GPUs with a per-step NCCL all-gather of the "
@@ -144,49 +148,245 @@ def feeds_for(w, steps, rank, seed):
             for i, node in enumerate(sorted(w.feeds))}
 
 
-def cpu_baseline(pm, neurons, sample_steps=20):
-    """The reference EngineCore<float> (oracle/_ref) on the box's host cores:
-    one single-row engine per thread (batch rows are independent), reference
-    protocol: warm-up, reset, timed run."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_planned(w, pm_repo):
+    """The reference planner's own plan of the config-4 graph (run_passes of the
+    unmodified reference, cached by oracle/make_ref_plan.py: it takes ~7 min),
+    as a reference PlannedModel; the repo's plan only if the cache is missing."""
+    from oracle import make_ref_plan, refapi
+    try:
+        pm, secs = make_ref_plan.load(w.model)
+        return refapi.planned_from_python(pm), f"reference run_passes (cached, {secs:.0f} s to plan)"
+    except Exception as ex:  # noqa: BLE001 - report which plan was used
+        return refapi.planned_from_python(pm_repo), f"repo planner (reference plan cache unavailable: {ex})"
+
+
+def cpu_baseline(rp, plan_note, neurons, sample_steps=20, seed=1):
+    """The reference engines (oracle/_ref: EngineCore<float> — the fp32 parity
+    oracle — and EngineCore<double>, what the reference's run_bench times) on the
+    box's host cores, reference protocol (warm-up run, reset, timed run;
+    bench.cpp:218-225), every feed slot driven by white noise as on the GPU:
+    all host threads (one single-row engine per thread; rows are independent)
+    and one core."""
     from oracle import refapi
     threads = os.cpu_count() or 1
-    secs = refapi.time_engines(pm, threads, 1, 1, sample_steps)
-    rows = threads
-    return {"value": rows * sample_steps * neurons / secs, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"{threads} batch rows x {sample_steps} timesteps of the config-4 network "
-                      f"({threads} single-row EngineCore<float>, one per host thread)",
-            "seconds": secs}
+    rate = {}
+    for fp64 in (False, True):
+        for n in (threads, 1):
+            secs = refapi.time_engines(rp, n, 1, sample_steps, sample_steps, fp64=fp64, feed_seed=seed)
+            rate[("f64" if fp64 else "f32", n)] = n * sample_steps * neurons / secs
+    return {"value": rate[("f32", threads)], "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{threads} batch rows x {sample_steps} timesteps of the config-4 network with white-noise "
+                      f"feeds ({threads} single-row EngineCore<float>, one per host thread), after a "
+                      f"{sample_steps}-step warm-up and reset",
+            "engine": "EngineCore<float> (oracle/_ref, unmodified reference sources, -O3 -DNDEBUG)",
+            "plan": plan_note, "cpu_model": cpu_model(),
+            "variants": {"f32_all_cores": rate[("f32", threads)], "f32_1_core": rate[("f32", 1)],
+                         "f64_all_cores": rate[("f64", threads)], "f64_1_core": rate[("f64", 1)]}}
 
 
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from paper_1805_11144_b200 import networks
-    w, pm, _ = build_workload(args, rank, args.batch)
-    neurons = networks.neuron_count(w.model)
     from oracle import refapi
+    from paper_1805_11144_b200 import networks, passes
+    w = networks.random_network(args.seed, 2048, 512, 8, 8, 256, args.batch, 1, name="config4_random_2048x512")
+    neurons = networks.neuron_count(w.model)
+    try:
+        from oracle import make_ref_plan
+        pm, psecs = make_ref_plan.load(w.model)
+        rp, plan_note = refapi.planned_from_python(pm), f"reference run_passes (cached, {psecs:.0f} s to plan)"
+    except Exception as ex:  # noqa: BLE001
+        rp = refapi.planned_from_python(passes.run_passes(w.model))
+        plan_note = f"repo planner (reference plan cache unavailable: {ex})"
     threads = os.cpu_count() or 1
-    rp = refapi.planned_from_python(pm)
     steps = max(args.steps // 100, 2)  # bounded sample: a few timesteps of `threads` rows
-    secs = refapi.time_engines(rp, threads, 1, max(args.warmup // 5, 1), steps)
+    warm = max(args.warmup // 5, 1)
+    secs = refapi.time_engines(rp, threads, 1, warm, steps, fp64=False, feed_seed=args.seed)
     value = threads * steps * neurons / secs
+    secs64 = refapi.time_engines(rp, threads, 1, warm, steps, fp64=True, feed_seed=args.seed)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
-            "warmup": max(args.warmup // 5, 1), "ms_per_step": 1e3 * secs / steps * (args.batch / threads),
+            "warmup": warm, "ms_per_step": 1e3 * secs / steps * (args.batch / threads),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": "config4_random_2048x512", "neurons": neurons, "batch": args.batch,
-                       "sample_rows": threads, "engine": "EngineCore<float> (oracle/_ref, unmodified sources)"},
+                       "sample_rows": threads, "engine": "EngineCore<float> (oracle/_ref, unmodified sources)",
+                       "plan": plan_note, "feeds": "white noise N(0,1) on all 256 inputs", "cpu_model": cpu_model()},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": f"{threads} rows x {steps} timesteps, one single-row engine per thread"},
+                             "sample": f"{threads} rows x {steps} timesteps, one single-row engine per thread",
+                             "f64_value": threads * steps * neurons / secs64},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+CONFIG_NAMES = {0: "config0_integrator", 1: "config1_cconv", 2: "config2_random_256x1024",
+                3: "config3_spiking_mlp", 4: "config4_random_2048x512"}
+
+
+def config_workload(cfg, steps):
+    from paper_1805_11144_b200 import networks
+    if cfg == 0:
+        return networks.config0(steps=steps)
+    if cfg == 1:
+        return networks.config1(steps=steps)
+    if cfg == 2:
+        return networks.config2(steps=steps)
+    if cfg == 3:
+        return networks.config3(steps=steps)
+    return networks.config4(steps=steps)
+
+
+def device_feeds(torch, w, steps, dev):
+    """The workload's host feeds ([B][S][dim] per node, tiled over `steps`) as the
+    run_device layout [slot][step][dim][B] f32 in HBM."""
+    B = w.batch
+    parts, ptrs = [], []
+    for fs in w.model.feed_slots:
+        x = w.feeds.get(fs.node_id)
+        if x is None:
+            x = np.zeros((B, 1, fs.dim))
+        reps = -(-steps // x.shape[1])
+        x = np.tile(x, (1, reps, 1))[:, :steps, :]
+        parts.append(np.ascontiguousarray(np.transpose(x, (1, 2, 0)), dtype=np.float32).ravel())
+    flat = torch.from_numpy(np.concatenate(parts) if parts else np.zeros(1, np.float32)).to(dev)
+    at = 0
+    for p_ in parts:
+        ptrs.append(flat.data_ptr() + 4 * at)
+        at += p_.size
+    return flat, ptrs
+
+
+def run_config(args):
+    """One BASELINE configuration other than config 4 on one GPU: device-resident
+    `value` (run_device, feeds in HBM) and `e2e` through neng_gpu_run with host f64
+    feeds and probes, next to the reference EngineCore<float> on the host cores."""
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    import torch
+    from paper_1805_11144_b200 import networks, passes
+    from paper_1805_11144_b200.engine import PRECISION_BF16X3, PRECISION_STRICT_FP32, PRECISION_TF32, GpuEngine
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    prec = {"fp32": PRECISION_STRICT_FP32, "tf32": PRECISION_TF32, "bf16x3": PRECISION_BF16X3}[args.precision]
+    K, W = args.steps, max(args.warmup, 3)
+    w = config_workload(args.config, max(K, W))
+    t0 = time.time()
+    pm = passes.run_passes(w.model)
+    plan_s = time.time() - t0
+    B = w.batch
+    neurons = networks.neuron_count(w.model)
+    eng = GpuEngine(pm, B, device=local, precision=prec)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    dims = [w.model.signals[p_.signal].size() for p_ in w.model.probes]
+
+    def ring(steps):
+        r = torch.empty(max(sum(dims) * steps * B, 1), dtype=torch.float32, device=dev)
+        ptrs, at = [], 0
+        for d in dims:
+            ptrs.append(r.data_ptr() + 4 * at)
+            at += d * steps * B
+        return r, ptrs
+
+    wf, wptr = device_feeds(torch, w, W, dev)
+    wr, wrp = ring(W)
+    eng.run_device(W, wptr, wrp, stream.cuda_stream)
+    tf, tptr = device_feeds(torch, w, K, dev)
+    tr, trp = ring(K)
+    eng.reset()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    eng.run_device(K, tptr, trp, stream.cuda_stream)
+    launches = eng.last_launch_count()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = ev0.elapsed_time(ev1)
+    clocks = sampler.stop()
+    steps_per_s = K / (ms / 1e3)
+    value = steps_per_s * neurons * B
+    # end to end: host f64 feeds in, f64 probes out through neng_gpu_run
+    hfeeds = {node: np.tile(x, (1, -(-K // x.shape[1]), 1))[:, :K, :] for node, x in w.feeds.items()}
+    eng.reset()
+    eng.run(K, hfeeds)
+    eng.reset()
+    torch.cuda.synchronize(dev)
+    t1 = time.perf_counter()
+    eng.run(K, hfeeds)
+    sec = time.perf_counter() - t1
+    h2d = sum(fs.dim for fs in w.model.feed_slots) * B * 4
+    d2h = sum(dims) * B * 4
+    e2e = {"value": K / sec * neurons * B, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "steps": K, "ms_per_step": 1e3 * sec / K,
+           "note": "neng_gpu_run: host f64 feeds -> f32 staging -> H2D -> kernels -> probe D2H -> f64"}
+    peak, peak_src = peaks()
+    bytes_step = networks.algorithmic_bytes_per_step(w.model, B)
+    launch_s = (ms / 1e3) / max(launches, 1)
+    roof = {"bound": "hbm", "achieved": bytes_step * (K / max(launches, 1)) / launch_s / 1e9, "peak": peak,
+            "unit": "GB/s", "peak_source": peak_src, "algorithmic_bytes_per_step": bytes_step}
+    roof["frac"] = roof["achieved"] / peak
+    if args.config == 3 and prec != PRECISION_STRICT_FP32:
+        flop_step = 2.0 * B * sum(w.model.signals[op.operands[0].signal].size() for op in w.model.operators
+                                  if op.kind.name == "DotInc")
+        tpk = {PRECISION_TF32: 0.5, PRECISION_BF16X3: 1.0 / 3.0}[prec] * _measured("bf16_tflops", 2250.0)
+        roof = {"bound": "tensor", "achieved": flop_step * steps_per_s / 1e12, "peak": tpk, "unit": "TFLOP/s",
+                "frac": flop_step * steps_per_s / 1e12 / tpk, "flop_per_step": flop_step,
+                "peak_source": "MEASURED_PEAKS bf16 dense x 1/2 (TF32 rate)" if prec == PRECISION_TF32
+                else "MEASURED_PEAKS bf16 dense x 1/3 (three bf16 MMAs per product)",
+                "hbm_frac": roof["frac"]}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": W,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if prec == PRECISION_STRICT_FP32 else args.precision, "data": "synthetic",
+            "config": {"workload": CONFIG_NAMES[args.config], "neurons": neurons, "batch": B,
+                       "operators": len(pm.model.operators), "groups_per_step": len(pm.plan),
+                       "plan_seconds": round(plan_s, 2), "mode": "fused" if eng.mode() == 2 else "generic",
+                       "precision": args.precision,
+                       "l2": "no flush: the per-step working set is what the configuration holds"},
+            "timesteps_per_sec": steps_per_s, "roofline": roof, "gpu_launches": launches, "clocks": clocks,
+            "e2e": e2e}
+    if not args.no_cpu_baseline:
+        from oracle import refapi
+        threads = os.cpu_count() or 1
+        rows = min(threads, B)
+        steps = 20 if neurons * B > 1e6 else 200
+        secs = refapi.time_engines(refapi.planned_from_python(pm), rows, 1, steps, steps, feed_seed=args.seed)
+        line["cpu_baseline"] = {"value": rows * steps * neurons / secs, "unit": UNIT, "cores": rows,
+                                "kind": "reference", "cpu_model": cpu_model(),
+                                "sample": f"{rows} single-row EngineCore<float> x {steps} timesteps (white-noise "
+                                          f"feeds), one per host thread"}
+    print(json.dumps(line), flush=True)
+
+
+def _measured(key, default):
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)[key])
+    except Exception:
+        return default
 
 
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference_arm(args)
+        return
+    if args.config != 4:
+        run_config(args)
         return
     rank, world, local = dist_env()
     import torch
@@ -338,8 +538,8 @@ def main():
     }
     if world == 1 and not args.no_cpu_baseline:
         try:
-            from oracle import refapi
-            line["cpu_baseline"] = cpu_baseline(refapi.planned_from_python(pm), neurons)
+            rp, plan_note = reference_planned(w, pm)
+            line["cpu_baseline"] = cpu_baseline(rp, plan_note, neurons, seed=args.seed)
         except Exception as ex:  # the oracle travels prebuilt; report rather than die
             line["cpu_baseline"] = {"error": str(ex)}
     print(json.dumps(line), flush=True)

@@ -11,7 +11,9 @@
 //   * validate_operators + build_dependency_graph + toposort_schedule
 //     (ir.cpp:310-317, 396-488)                        -> nref_validate / nref_toposort
 // Models cross as the same POD views the product ABI uses (include/neng_gpu.h).
+#include <algorithm>
 #include <chrono>
+#include <random>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -426,37 +428,80 @@ neng_status nref_run_reference(const neng_built_model* m, int32_t n_steps, int32
 /// (warm-up run, reset, timed run — bench.cpp:218-225). Batch rows are
 /// independent (test_exec.cpp:246-267), so splitting them across engines is
 /// exact. Returns the wall seconds of the timed run (max over threads).
+}  // extern "C"
+
+namespace {
+
+template <class T>
+double time_engines_t(const nref_planned* p, int threads, int rows, int warm_steps, int timed_steps,
+                      uint64_t feed_seed) {
+    // white-noise feeds N(0, 1) for every feed slot, per engine (seeded, generated before timing)
+    const neng::BuiltModel& m = p->pm.model;
+    const int steps = std::max(std::max(warm_steps, timed_steps), 1);
+    std::vector<neng::FeedData> feeds(threads);
+    if (feed_seed)
+        for (int t = 0; t < threads; ++t) {
+            std::mt19937_64 rng(feed_seed + 1000003ull * t);
+            std::normal_distribution<double> nd(0.0, 1.0);
+            for (const neng::FeedSlot& fs : m.feed_slots) {
+                neng::Tensor3 x(rows, steps, fs.dim);
+                for (double& v : x.data) v = nd(rng);
+                feeds[t].emplace(fs.node_id, std::move(x));
+            }
+        }
+    std::vector<std::unique_ptr<neng::EngineCore<T>>> engines(threads);
+    std::vector<std::thread> pool;
+    std::vector<double> secs(threads, 0.0);
+    std::vector<std::string> errs(threads);
+    for (int t = 0; t < threads; ++t)
+        pool.emplace_back([&, t] {
+            try {
+                engines[t] = std::make_unique<neng::EngineCore<T>>(p->pm, rows, 1);
+                if (warm_steps > 0) engines[t]->run(warm_steps, feeds[t]);  // warm-up, excluded (bench.cpp:221)
+                engines[t]->reset();
+            } catch (const std::exception& ex) {
+                errs[t] = ex.what();
+            }
+        });
+    for (auto& th : pool) th.join();
+    for (auto& s : errs)
+        if (!s.empty()) throw neng::RunError(s);
+    pool.clear();
+    for (int t = 0; t < threads; ++t)
+        pool.emplace_back([&, t] {
+            try {
+                auto t0 = std::chrono::steady_clock::now();
+                engines[t]->run(timed_steps, feeds[t]);
+                secs[t] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            } catch (const std::exception& ex) {
+                errs[t] = ex.what();
+            }
+        });
+    for (auto& th : pool) th.join();
+    for (auto& s : errs)
+        if (!s.empty()) throw neng::RunError(s);
+    double mx = 0.0;
+    for (double s : secs) mx = std::max(mx, s);
+    return mx;
+}
+
+}  // namespace
+
+extern "C" {
+
 neng_status nref_time_engines(const nref_planned* p, int32_t threads, int32_t rows_per_engine,
                               int32_t warm_steps, int32_t timed_steps, double* seconds_out) {
+    return guarded([&] { *seconds_out = time_engines_t<float>(p, threads, rows_per_engine, warm_steps, timed_steps, 0); });
+}
+
+/// nref_time_engines with the engine precision (fp64: EngineCore<double>, what the
+/// reference's run_bench times, bench.cpp:218) and seeded white-noise feeds on every
+/// feed slot (feed_seed 0: no feeds).
+neng_status nref_time_engines2(const nref_planned* p, int32_t threads, int32_t rows_per_engine, int32_t warm_steps,
+                               int32_t timed_steps, int32_t fp64, uint64_t feed_seed, double* seconds_out) {
     return guarded([&] {
-        std::vector<std::unique_ptr<neng::EngineCore<float>>> engines(threads);
-        std::vector<std::thread> pool;
-        std::vector<double> secs(threads, 0.0);
-        std::vector<std::string> errs(threads);
-        for (int t = 0; t < threads; ++t)
-            pool.emplace_back([&, t] {
-                try {
-                    engines[t] = std::make_unique<neng::EngineCore<float>>(p->pm, rows_per_engine, 1);
-                    if (warm_steps > 0) engines[t]->run(warm_steps);
-                    engines[t]->reset();
-                } catch (const std::exception& ex) {
-                    errs[t] = ex.what();
-                }
-            });
-        for (auto& th : pool) th.join();
-        for (auto& s : errs)
-            if (!s.empty()) throw neng::RunError(s);
-        pool.clear();
-        for (int t = 0; t < threads; ++t)
-            pool.emplace_back([&, t] {
-                auto t0 = std::chrono::steady_clock::now();
-                engines[t]->run(timed_steps);
-                secs[t] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-            });
-        for (auto& th : pool) th.join();
-        double mx = 0.0;
-        for (double s : secs) mx = std::max(mx, s);
-        *seconds_out = mx;
+        *seconds_out = fp64 ? time_engines_t<double>(p, threads, rows_per_engine, warm_steps, timed_steps, feed_seed)
+                            : time_engines_t<float>(p, threads, rows_per_engine, warm_steps, timed_steps, feed_seed);
     });
 }
 

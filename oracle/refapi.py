@@ -228,15 +228,20 @@ def run_reference(model: ir.BuiltModel, n_steps: int, feeds=None, minibatch: int
     return _abi.split_probes(model, out, minibatch, n_steps)
 
 
-def time_engines(planned, threads: int, rows_per_engine: int, warm_steps: int, timed_steps: int) -> float:
-    """Wall seconds for `threads` parallel EngineCore<float> engines of
-    `rows_per_engine` rows each to advance `timed_steps` (reference protocol:
-    warm-up, reset, timed run)."""
+def time_engines(planned, threads: int, rows_per_engine: int, warm_steps: int, timed_steps: int,
+                 fp64: bool = False, feed_seed: int = 0) -> float:
+    """Wall seconds (max over threads) for `threads` parallel reference engines
+    (EngineCore<float>, or EngineCore<double> with fp64) of `rows_per_engine`
+    rows each to advance `timed_steps` (reference protocol, bench.cpp:218-225:
+    warm-up run, reset, timed run), every feed slot driven by seeded N(0, 1)
+    white noise when feed_seed != 0."""
     lib = ref_lib()
     rp = _as_ref_planned(planned)
     secs = C.c_double()
-    _check(lib, lib.nref_time_engines(C.c_void_p(rp.h), threads, rows_per_engine, warm_steps,
-                                      timed_steps, C.byref(secs)))
+    lib.nref_time_engines2.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                       C.c_uint64, C.POINTER(C.c_double)]
+    _check(lib, lib.nref_time_engines2(C.c_void_p(rp.h), threads, rows_per_engine, warm_steps, timed_steps,
+                                       int(fp64), feed_seed, C.byref(secs)))
     return secs.value
 
 

@@ -78,3 +78,13 @@ def test_config4_graph_plans_in_seconds():
     # every group is single-kind and the plan is valid for the reference's own checker
     kinds = {o.id: o.kind for o in pm.model.operators}
     assert all(len({kinds[i] for i in g}) == 1 for g in pm.plan)
+
+
+def test_config4_plan_identical_to_the_reference_planners():
+    """Plan identity at config-4 scale: the repo planner's plan of the 78,849-
+    operator graph equals the plan the reference's own run_passes produced
+    (cached by oracle/make_ref_plan.py — the reference needs ~7 min for it)."""
+    from oracle import make_ref_plan
+    w = networks.random_network(1, 2048, 512, 8, 8, 256, 1, 1, name="config4_random_2048x512")
+    ref, _ = make_ref_plan.load(w.model)  # raises if the cache was planned for another model
+    same_plan(passes.run_passes(w.model), ref)
