@@ -633,6 +633,7 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             x.ds = m.signals[c.src].rows();
             x.src_feed = -1;
             x.src_xb = ens_of_xhat.count(c.src) ? fe[ens_of_xhat.at(c.src)].xb_row : -1;
+            x.src_ens = ens_of_xhat.count(c.src) ? ens_of_xhat.at(c.src) : -1;
             if (c.dst_ens < 0) orphans.push_back(static_cast<int32_t>(fc.size()));
             if ((c.dst_ens < 0 && R == 0) || (c.dst_ens >= ens_lo && c.dst_ens < ens_hi))
                 my_conns.push_back(static_cast<int32_t>(fc.size()));

@@ -251,7 +251,7 @@ __device__ Smem carve(uint32_t* base, const FusedProgram& p) {
 }
 
 template <int DMAX>
-size_t smem_bytes(const FusedProgram& p) {
+__host__ __device__ size_t smem_bytes(const FusedProgram& p) {
     return 128 + static_cast<size_t>(kWarps) * kRingFloats * 4 + inq_bytes<DMAX>(p) +
            static_cast<size_t>(p.nmax) * DMAX * 4 + static_cast<size_t>(p.nmax) * 4 +
            static_cast<size_t>(p.stage_dec ? p.pmax_floats : 0) * 4 + static_cast<size_t>(p.tu) * p.nmax * 4;
@@ -270,13 +270,6 @@ __device__ __forceinline__ int batch_of(const FusedProgram& p) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-// L2 policy: the streamed neuron state is evict-first, so the libm tables the
-// queue batches probe (a few MB) stay L2-resident next to 2 GB/step of v, r
-__device__ __forceinline__ uint64_t l2_evict_first() {
-    uint64_t pol;
-    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
 // No L2::cache_hint operand on cp.async: for some kernel shapes (the BT = 0
 // instances) ptxas 12.9 encodes the hinted LDGSTS with its 64-bit memory
 // descriptor in an odd uniform register (desc[UR1]), which faults at run time
@@ -405,6 +398,12 @@ __device__ __forceinline__ int exc_batch(const FusedProgram& p, const FEns* ep, 
     const bool d = on && doubtful;
     const uint32_t m = __ballot_sync(kFull, d);
     if (d) qd[nd + __popc(m & lanemask_lt())] = x;
+#ifdef NENG_FUSED_CHECKS
+    if (nd + __popc(m) > kQ) {
+        printf("fused check: doubt queue overflow %d\n", nd + __popc(m));
+        __trap();
+    }
+#endif
     return nd + __popc(m);
 }
 
@@ -677,6 +676,18 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
         for (int q = 0; q < e.inc_count; ++q) {
             const FConn& cn = p.conns[__ldg(p.incoming + e.inc_begin + q)];
             float f[DMAX];
+#ifdef NENG_FUSED_CHECKS
+            // checked builds: the barrier-free schedule's claim on the source's step k-1 xhat —
+            // the source unit has finished step k-1 (done >= t) and has not yet finished step
+            // k+2, which rewrites slot (k-1) % 3 (done <= t + 2)
+            if (df_pos >= 0 && do_update && cn.src_ens >= 0 && lane == 0) {
+                const int seen = ld_acquire(p.done + static_cast<int64_t>(cn.src_ens - p.ens_lo) * p.groups + g);
+                if (seen < df_t || seen > df_t + 2) {
+                    printf("fused check: unit %d step %d reads ensemble %d's xhat at done=%d\n", u, k, cn.src_ens, seen);
+                    __trap();
+                }
+            }
+#endif
             if (do_update) {
                 conn_rows<DMAX, BT>(p, cn, k - 1, b, r_lo, r_hi, valid, false, f);
             } else {
@@ -862,6 +873,12 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
                 const uint32_t me = __ballot_sync(kFull, xq);
                 if (xq) qe[ne + __popc(me & lt_mask)] = QEnt{key, h ? v2.y : v2.x, rh, J};
                 ne += __popc(me);
+#ifdef NENG_FUSED_CHECKS
+                if (ne > kQ || nd > kQ) {
+                    printf("fused check: queue overflow ne=%d nd=%d\n", ne, nd);
+                    __trap();
+                }
+#endif
                 // warp-uniform drains; a row adds <= 32 entries, so ne < 32 before a row
                 if (ne >= 32) {
                     ne -= 32;
@@ -1027,6 +1044,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fused_run_kernel(const _
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(128) uint32_t smem[];
     const Smem S = carve<DMAX>(smem, p);
+#ifdef NENG_FUSED_CHECKS
+    {
+        uint32_t dyn;
+        asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+        if (threadIdx.x == 0 && smem_bytes<DMAX>(p) > dyn) {
+            printf("fused check: carve needs %llu of %u bytes\n", (unsigned long long)smem_bytes<DMAX>(p), dyn);
+            __trap();
+        }
+    }
+#endif
     if (threadIdx.x == 0) {
         mbar_init(S.bar);
         mbar_init(S.bar2);

@@ -66,6 +66,7 @@ struct FConn {
     int64_t acc_base, filt_base, state_base;
     int32_t dd, ds;
     int32_t src_xb;    // first parity-buffer row of the source ensemble's xhat, or -1
+    int32_t src_ens;   // the source ensemble (global index), or -1
     int32_t src_feed;  // feed slot index when the source is a fed node, else -1
     int32_t acc_init_off;
     int32_t probe_filt, probe_state;  // probe indices capturing filt / state, -1 none
