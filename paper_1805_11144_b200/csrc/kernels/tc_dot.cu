@@ -119,7 +119,8 @@ struct Geo {
     static constexpr int kXBytes = kChunks * kXChunkBytes;     // X tile of one stage (per half)
     static constexpr int kHalves = MODE == TC_TF32 ? 1 : 2;
     static constexpr int kStageBytes = kHalves * (kABytes + kXBytes);
-    static constexpr int kStages = MODE == TC_TF32 ? 4 : 3;
+    // as many stages as fit ~200 KB: the k loop is latency-bound on the TMA round trip at these sizes
+    static constexpr int kStages = (200 * 1024 / kStageBytes) < 8 ? (200 * 1024 / kStageBytes) : 8;
     static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes + 256;
     static_assert(BN % kChunk == 0, "BN must be a whole number of 128-byte chunks");
 };
