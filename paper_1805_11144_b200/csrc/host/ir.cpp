@@ -167,150 +167,143 @@ namespace {
     throw StructuralError(os.str());
 }
 
-void expect_arity(const Operator& op, size_t n) {
-    if (op.operands.size() != n)
-        structural_fail(op, "expected " + std::to_string(n) + " operands, got " +
-                                std::to_string(op.operands.size()));
-}
+/// The operand signature of an operator kind: how many operands it takes and
+/// how it accesses each (the reference's table, ir.cpp:130-167).  Positions
+/// past the table read as Update (SimNeurons' state operands).
+struct Signature {
+    size_t arity;
+    std::vector<AccessMode> modes;
+};
 
-}  // namespace
-
-// operand_modes (ir.cpp:130-167)
-std::vector<std::pair<int, AccessMode>> operand_modes(const Operator& op) {
+Signature signature_of(const Operator& op) {
     using M = AccessMode;
     switch (op.kind) {
-        case OpKind::Reset:
-            expect_arity(op, 1);
-            return {{0, M::Set}};
-        case OpKind::Copy:
-            expect_arity(op, 2);
-            return {{0, M::Read}, {1, op.inc ? M::Inc : M::Set}};
+        case OpKind::Reset: return {1, {M::Set}};
+        case OpKind::Copy: return {2, {M::Read, op.inc ? M::Inc : M::Set}};
         case OpKind::ElementwiseInc:
-        case OpKind::DotInc:
-            expect_arity(op, 3);
-            return {{0, M::Read}, {1, M::Read}, {2, M::Inc}};
-        case OpKind::SimNeurons: {
-            expect_arity(op, op.neuron.has_state() ? 4 : 2);
-            std::vector<std::pair<int, M>> m = {{0, M::Read}, {1, M::Set}};
-            for (size_t i = 2; i < op.operands.size(); ++i) m.emplace_back(static_cast<int>(i), M::Update);
-            return m;
-        }
+        case OpKind::DotInc: return {3, {M::Read, M::Read, M::Inc}};
+        case OpKind::SimNeurons: return {op.neuron.has_state() ? size_t{4} : size_t{2}, {M::Read, M::Set}};
         case OpKind::SimProcess:
-            if (op.tau > 0.0) {
-                expect_arity(op, 3);
-                return {{0, M::Read}, {1, M::Update}, {2, M::Update}};
-            }
-            expect_arity(op, 2);
-            return {{0, M::Read}, {1, M::Set}};
-        case OpKind::SimPES:
-            expect_arity(op, 3);
-            return {{0, M::Read}, {1, M::Read}, {2, M::Update}};
-        case OpKind::TimeUpdate:
-            expect_arity(op, 2);
-            return {{0, M::Update}, {1, M::Update}};
+            return op.tau > 0.0 ? Signature{3, {M::Read, M::Update, M::Update}} : Signature{2, {M::Read, M::Set}};
+        case OpKind::SimPES: return {3, {M::Read, M::Read, M::Update}};
+        case OpKind::TimeUpdate: return {2, {M::Update, M::Update}};
     }
     structural_fail(op, "unknown kind");
 }
 
+}  // namespace
+
+std::vector<std::pair<int, AccessMode>> operand_modes(const Operator& op) {
+    const Signature sg = signature_of(op);
+    if (op.operands.size() != sg.arity)
+        structural_fail(op, "expected " + std::to_string(sg.arity) + " operands, got " +
+                                std::to_string(op.operands.size()));
+    std::vector<std::pair<int, AccessMode>> out;
+    out.reserve(sg.arity);
+    for (size_t i = 0; i < sg.arity; ++i)
+        out.emplace_back(static_cast<int>(i), i < sg.modes.size() ? sg.modes[i] : AccessMode::Update);
+    return out;
+}
+
 namespace {
 
-const Signal& ref_signal(const std::vector<Signal>& signals, const Operator& op, const SignalRef& r) {
-    if (r.signal < 0 || static_cast<size_t>(r.signal) >= signals.size())
-        structural_fail(op, "ref to unknown signal " + std::to_string(r.signal));
-    return signals[r.signal];
-}
+/// Structural checks of one operator against the signal table; every failure
+/// is a StructuralError naming the operator (messages as the reference's,
+/// ir.cpp:228-306, which the tests compare).
+class OperandCheck {
+public:
+    OperandCheck(const std::vector<Signal>& signals, const Operator& op) : sig_(signals), op_(op) {}
 
-void check_ref(const std::vector<Signal>& signals, const Operator& op, const SignalRef& r) {
-    const Signal& s = ref_signal(signals, op, r);
-    if (r.start < 0 || r.stop > s.rows() || r.start >= r.stop)
-        structural_fail(op, "slice [" + std::to_string(r.start) + ", " + std::to_string(r.stop) +
-                                ") out of bounds for signal '" + s.label + "' with " +
-                                std::to_string(s.rows()) + " rows");
-}
-
-bool is_scalar_ref(const std::vector<Signal>& signals, const SignalRef& r) {
-    return r.rows() == 1 && signals[r.signal].elems_per_row() == 1;
-}
-
-long long ref_elems(const std::vector<Signal>& signals, const SignalRef& r) {
-    return static_cast<long long>(r.rows()) * signals[r.signal].elems_per_row();
-}
-
-void same_layout(const std::vector<Signal>& signals, const Operator& op, const SignalRef& a, const SignalRef& b,
-                 const char* what) {
-    if (a.rows() != b.rows() || signals[a.signal].trailing_shape() != signals[b.signal].trailing_shape())
-        structural_fail(op, std::string(what) + " shapes do not agree");
-}
-
-void rank1(const std::vector<Signal>& signals, const Operator& op, const SignalRef& r, const char* what) {
-    if (!signals[r.signal].trailing_shape().empty())
-        structural_fail(op, std::string(what) + " must be a vector signal");
-}
-
-// validate_one (ir.cpp:228-306)
-void validate_one(const std::vector<Signal>& signals, const Operator& op) {
-    auto modes = operand_modes(op);
-    for (const SignalRef& r : op.operands) check_ref(signals, op, r);
-    int32_t elem = signals[op.operands[0].signal].elem;
-    for (const SignalRef& r : op.operands)
-        if (signals[r.signal].elem != elem) structural_fail(op, "operands mix element widths");
-    for (auto [pos, mode] : modes) {
-        if (mode == AccessMode::Read) continue;
-        const Signal& s = signals[op.operands[pos].signal];
-        if (s.constant) structural_fail(op, "writes constant signal '" + s.label + "'");
+    void run() {
+        const auto modes = operand_modes(op_);
+        for (const SignalRef& r : op_.operands) in_bounds(r);
+        const int32_t width = sig_[op_.operands[0].signal].elem;
+        require(std::all_of(op_.operands.begin(), op_.operands.end(),
+                            [&](const SignalRef& r) { return sig_[r.signal].elem == width; }),
+                "operands mix element widths");
+        for (auto [pos, mode] : modes) {
+            const Signal& s = sig_[op_.operands[pos].signal];
+            if (mode != AccessMode::Read && s.constant) fail("writes constant signal '" + s.label + "'");
+        }
+        kind_rules();
     }
-    switch (op.kind) {
-        case OpKind::Reset:
-            if (static_cast<long long>(op.value.size()) != ref_elems(signals, op.operands[0]))
-                structural_fail(op, "value length does not match destination");
-            break;
-        case OpKind::Copy:
-            same_layout(signals, op, op.operands[0], op.operands[1], "src/dst");
-            break;
-        case OpKind::ElementwiseInc: {
-            const SignalRef &a = op.operands[0], &x = op.operands[1], &y = op.operands[2];
-            same_layout(signals, op, x, y, "x/y");
-            if (!is_scalar_ref(signals, a)) same_layout(signals, op, a, x, "a/x");
-            break;
-        }
-        case OpKind::DotInc: {
-            const SignalRef &a = op.operands[0], &x = op.operands[1], &y = op.operands[2];
-            auto at = signals[a.signal].trailing_shape();
-            if (at.size() != 1) structural_fail(op, "a must be a matrix signal");
-            rank1(signals, op, x, "x");
-            rank1(signals, op, y, "y");
-            if (at[0] != x.rows()) structural_fail(op, "a columns do not match x rows");
-            if (a.rows() != y.rows()) structural_fail(op, "a rows do not match y rows");
-            if (refs_overlap(y, x) || refs_overlap(y, a)) structural_fail(op, "y aliases an input operand");
-            break;
-        }
-        case OpKind::SimNeurons: {
-            for (const SignalRef& r : op.operands) rank1(signals, op, r, "operand");
-            int n = op.operands[0].rows();
-            for (const SignalRef& r : op.operands)
-                if (r.rows() != n) structural_fail(op, "operand row counts differ");
-            break;
-        }
-        case OpKind::SimProcess:
-            same_layout(signals, op, op.operands[0], op.operands[1], "in/out");
-            if (op.operands.size() == 3) same_layout(signals, op, op.operands[1], op.operands[2], "out/state");
-            break;
-        case OpKind::SimPES: {
-            const SignalRef &pre = op.operands[0], &err = op.operands[1], &w = op.operands[2];
-            rank1(signals, op, pre, "pre");
-            rank1(signals, op, err, "error");
-            auto wt = signals[w.signal].trailing_shape();
-            if (wt.size() != 1) structural_fail(op, "weights must be a matrix signal");
-            if (w.rows() != err.rows() || wt[0] != pre.rows())
-                structural_fail(op, "weights shape does not match error x pre");
-            break;
-        }
-        case OpKind::TimeUpdate:
-            for (const SignalRef& r : op.operands)
-                if (ref_elems(signals, r) != 1) structural_fail(op, "step/time must be scalar signals");
-            break;
+
+private:
+    [[noreturn]] void fail(const std::string& what) const { structural_fail(op_, what); }
+    void require(bool ok, const std::string& what) const {
+        if (!ok) fail(what);
     }
-}
+    const SignalRef& arg(size_t i) const { return op_.operands[i]; }
+    std::vector<int> trailing(const SignalRef& r) const { return sig_[r.signal].trailing_shape(); }
+    long long elems(const SignalRef& r) const {
+        return static_cast<long long>(r.rows()) * sig_[r.signal].elems_per_row();
+    }
+
+    void in_bounds(const SignalRef& r) const {
+        require(r.signal >= 0 && static_cast<size_t>(r.signal) < sig_.size(),
+                "ref to unknown signal " + std::to_string(r.signal));
+        const Signal& s = sig_[r.signal];
+        require(r.start >= 0 && r.stop <= s.rows() && r.start < r.stop,
+                "slice [" + std::to_string(r.start) + ", " + std::to_string(r.stop) + ") out of bounds for signal '" +
+                    s.label + "' with " + std::to_string(s.rows()) + " rows");
+    }
+    void same_shape(const SignalRef& a, const SignalRef& b, const char* pair) const {
+        require(a.rows() == b.rows() && trailing(a) == trailing(b), std::string(pair) + " shapes do not agree");
+    }
+    void is_vector(const SignalRef& r, const char* what) const {
+        require(trailing(r).empty(), std::string(what) + " must be a vector signal");
+    }
+
+    void kind_rules() const {
+        switch (op_.kind) {
+            case OpKind::Reset:
+                require(static_cast<long long>(op_.value.size()) == elems(arg(0)),
+                        "value length does not match destination");
+                return;
+            case OpKind::Copy: same_shape(arg(0), arg(1), "src/dst"); return;
+            case OpKind::ElementwiseInc:
+                same_shape(arg(1), arg(2), "x/y");
+                if (!(arg(0).rows() == 1 && sig_[arg(0).signal].elems_per_row() == 1))  // a scalar scale broadcasts
+                    same_shape(arg(0), arg(1), "a/x");
+                return;
+            case OpKind::DotInc: {
+                const std::vector<int> at = trailing(arg(0));
+                require(at.size() == 1, "a must be a matrix signal");
+                is_vector(arg(1), "x");
+                is_vector(arg(2), "y");
+                require(at[0] == arg(1).rows(), "a columns do not match x rows");
+                require(arg(0).rows() == arg(2).rows(), "a rows do not match y rows");
+                require(!refs_overlap(arg(2), arg(1)) && !refs_overlap(arg(2), arg(0)), "y aliases an input operand");
+                return;
+            }
+            case OpKind::SimNeurons:
+                for (const SignalRef& r : op_.operands) is_vector(r, "operand");
+                for (const SignalRef& r : op_.operands) require(r.rows() == arg(0).rows(), "operand row counts differ");
+                return;
+            case OpKind::SimProcess:
+                same_shape(arg(0), arg(1), "in/out");
+                if (op_.operands.size() == 3) same_shape(arg(1), arg(2), "out/state");
+                return;
+            case OpKind::SimPES: {
+                is_vector(arg(0), "pre");
+                is_vector(arg(1), "error");
+                const std::vector<int> wt = trailing(arg(2));
+                require(wt.size() == 1, "weights must be a matrix signal");
+                require(arg(2).rows() == arg(1).rows() && wt[0] == arg(0).rows(),
+                        "weights shape does not match error x pre");
+                return;
+            }
+            case OpKind::TimeUpdate:
+                for (const SignalRef& r : op_.operands) require(elems(r) == 1, "step/time must be scalar signals");
+                return;
+        }
+    }
+
+    const std::vector<Signal>& sig_;
+    const Operator& op_;
+};
+
+void validate_one(const std::vector<Signal>& signals, const Operator& op) { OperandCheck(signals, op).run(); }
 
 // phase_edge (ir.cpp:351-360): Set < Inc < Read < Update, no Update -> Read.
 bool phase_edge(AccessMode from, AccessMode to) {

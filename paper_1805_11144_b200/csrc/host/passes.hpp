@@ -1,5 +1,6 @@
 // passes.hpp — the build-time passes that produce a PlannedModel
-// (semantics of proj/src/passes.cpp; see passes.cpp for the design).
+// (semantics of proj/src/passes.cpp): simplify and merge planning in
+// passes.cpp, the signal layout in layout.cpp.
 #pragma once
 
 #include "host_ir.hpp"
@@ -7,7 +8,6 @@
 namespace nengb {
 
 std::vector<Operator> simplify_operators(const std::vector<Signal>& signals, std::vector<Operator> ops);
-bool mergeable(const std::vector<Signal>& signals, const Operator& a, const Operator& b);
 Plan plan_tree_search(const std::vector<Signal>& signals, const std::vector<Operator>& ops, int depth);
 Plan plan_greedy(const std::vector<Signal>& signals, const std::vector<Operator>& ops);
 void validate_plan(const std::vector<Signal>& signals, const std::vector<Operator>& ops, const Plan& plan);
