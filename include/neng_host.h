@@ -36,6 +36,13 @@ void neng_plan_stats(const neng_plan* p, double* contiguous_read_fraction, int64
                      int32_t* groups_per_step);
 void neng_plan_destroy(neng_plan* p);
 
+/* solve_decoders (frontend.cpp:56-76) without Eigen: D solves
+ * (A^T A + m sigma^2 I) D = A^T Y with sigma = reg * max|A|; A [m][n], Y [m][d],
+ * decoders_out [n][d], all row-major doubles.  BuildError for an empty system,
+ * negative reg, or singular normal equations (reg too small). */
+neng_status neng_solve_decoders(const double* a, int32_t m, int32_t n, const double* y, int32_t d, double reg,
+                                double* decoders_out);
+
 /* Diagnostics: evaluate the device's glibc-parity expm1f (func 0) or log1pf
  * (func 1) on every float whose bit pattern is in [lo, lo + n); out_host gets
  * the result bit patterns. */

@@ -85,6 +85,15 @@ neng_status neng_model_dependency_edges(const neng_built_model* model, int64_t* 
     });
 }
 
+neng_status neng_solve_decoders(const double* a, int32_t m, int32_t n, const double* y, int32_t d, double reg,
+                                double* decoders_out) {
+    return guarded([&] {
+        if (!a || !y || !decoders_out) throw nengb::InvalidArgument("neng_solve_decoders: null argument");
+        const std::vector<double> dec = nengb::solve_decoders(a, m, n, y, d, reg);
+        std::memcpy(decoders_out, dec.data(), dec.size() * sizeof(double));
+    });
+}
+
 neng_status neng_run_passes(const neng_built_model* model, int32_t merge, int32_t simplify, int32_t planner,
                             int32_t tree_depth, int32_t sort, neng_plan** out) {
     return guarded([&] {

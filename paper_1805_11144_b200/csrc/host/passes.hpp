@@ -21,4 +21,7 @@ ContiguityStats contiguity_stats(const std::vector<ReadBlock>& blocks, const Buf
                                  const Plan& plan);
 PlannedModel run_passes(BuiltModel model, const PipelineConfig& config = {});
 
+// decoders.cpp: the frontend's regularised least-squares decoder solve (frontend.cpp:56-76)
+std::vector<double> solve_decoders(const double* A, int m, int n, const double* Y, int d, double reg);
+
 }  // namespace nengb

@@ -111,6 +111,36 @@ class NetBuilder:
         self.ens.append(e)
         return e
 
+    def solve_decoders(self, e: Ens, fn=None, fn_dim: Optional[int] = None, eval_points_per_dim: int = 500,
+                       radius: float = 1.0, reg: float = 0.1, tau_rc: float = 0.02, tau_ref: float = 0.002,
+                       amplitude: float = 1.0) -> np.ndarray:
+        """Least-squares decoders of f(x) for LIF ensemble e (Lowering::decode,
+        frontend.cpp:376-417): eval points uniform in the radius-ball (seeded
+        directions, radius * U^(1/d)), activities = the LIF rate of the
+        ensemble's own encoders and biases, and the native Eigen-free solve
+        (passes.solve_decoders).  Returns D [fn_dim][n] (the decoded()
+        layout); fn maps a [m][d] array of points to [m][fn_dim] (default:
+        the identity)."""
+        from . import passes
+        E = np.asarray(self.m.signals[e.enc].initial).reshape(e.n, e.d)  # gain / radius folded in
+        bias = next(np.asarray(op.value) for op in self.m.operators
+                    if op.kind == ir.OpKind.Reset and op.operands[0].signal == e.j)
+        m = eval_points_per_dim * e.d
+        rng = Rng(derive_seed(self.seed, 2 * e.index + 1))
+        pts = np.empty((m, e.d))
+        for s_ in range(m):  # reference order: d normals then one uniform per point
+            x = np.array([rng.gaussian() for _ in range(e.d)])
+            r = radius * rng.uniform() ** (1.0 / e.d)
+            nsq = float(x @ x)
+            pts[s_] = x * (0.0 if nsq < 1e-24 else r / math.sqrt(nsq))
+        J = pts @ E.T + bias[None, :]
+        with np.errstate(divide="ignore"):
+            act = np.where(J > 1.0, amplitude / (tau_ref + tau_rc * np.log1p(1.0 / np.maximum(J - 1.0, 1e-300))), 0.0)
+        Y = pts if fn is None else np.asarray(fn(pts), dtype=np.float64).reshape(m, -1)
+        if fn_dim is not None and Y.shape[1] != fn_dim:
+            raise ValueError(f"function returned {Y.shape[1]} values, expected {fn_dim}")
+        return passes.solve_decoders(act, Y, reg).T
+
     def decoded(self, e: Ens, D: np.ndarray) -> int:
         """Decoded value xhat = D . out (D: d_out x n), SURVEY §8(d) unfolded lowering."""
         D = np.asarray(D, dtype=np.float64)
@@ -292,13 +322,15 @@ def random_network(seed: int, n_ens: int, n: int, d: int, k_out: int, n_inputs: 
     return Workload(name, nb.m, batch, steps, feeds, n_ens * n)
 
 
-def config1(seed: int = 1, steps: int = 1000, batch: int = 64, dims: int = 64) -> Workload:
+def config1(seed: int = 1, steps: int = 1000, batch: int = 64, dims: int = 64, decoders: str = "ls") -> Workload:
     """Circular convolution of two `dims`-D inputs (BASELINE config 1): per batch row
     seeded unit-norm Gaussian vectors A, B, constant over the run.  The real DFT
     (frequencies 0..dims/2) projects A and B into 4*(dims/2+1) two-D product
     ensembles (100 LIF each; inputs [row_a.A, row_b.B] for the re*re, im*im,
-    re*im, im*re products of each frequency); the product decoders are seeded
-    N(0, 1/100) (BASELINE leaves them unspecified; no least-squares solve); the
+    re*im, im*re products of each frequency); the product decoders (BASELINE
+    leaves them unspecified) are the least-squares decoders of x0 * x1
+    (decoders="ls", NetBuilder.solve_decoders: the frontend's regularised solve
+    without Eigen), or seeded N(0, 1/100) with decoders="random"; the
     inverse real DFT maps the products onto `dims` one-D output ensembles (50
     LIF each) as scalar-transform decoded connections.  Every synapse is a
     lowpass with tau = 0.005 s.  Probes: the first four output ensembles'
@@ -321,7 +353,11 @@ def config1(seed: int = 1, steps: int = 1000, batch: int = 64, dims: int = 64) -
                 nb.connect(a, e.in_, np.vstack([ra[k], np.zeros(d)]), synapse=0.005)
             if np.any(rb[k] != 0.0):
                 nb.connect(b, e.in_, np.vstack([np.zeros(d), rb[k]]), synapse=0.005)
-            nb.decoded(e, rng.normal(0.0, math.sqrt(1.0 / 100), size=(1, 100)))
+            if decoders == "ls":  # the product x0 * x1, least squares over the radius-1.5 ball (covers [-1, 1]^2)
+                D = nb.solve_decoders(e, lambda p: p[:, :1] * p[:, 1:2], 1, eval_points_per_dim=100, radius=1.5)
+            else:
+                D = rng.normal(0.0, math.sqrt(1.0 / 100), size=(1, 100))
+            nb.decoded(e, D)
             prods.append((e, k, typ))
     outs = []
     for j in range(d):

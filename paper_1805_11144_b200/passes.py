@@ -31,6 +31,8 @@ def lib():
         L.neng_model_dependency_edges.argtypes = [C.POINTER(_abi.neng_built_model), C.POINTER(C.c_int64),
                                                   C.POINTER(C.c_int32)]
         L.neng_debug_libm_eval.argtypes = [C.c_int32, C.c_int32, C.c_uint32, C.c_int64, C.POINTER(C.c_uint32)]
+        L.neng_solve_decoders.argtypes = [C.POINTER(C.c_double), C.c_int32, C.c_int32, C.POINTER(C.c_double),
+                                          C.c_int32, C.c_double, C.POINTER(C.c_double)]
         _configured = True
     return L
 
@@ -85,3 +87,23 @@ def debug_libm_eval(func: int, lo: int, n: int, device: int = 0) -> np.ndarray:
     out = np.zeros(max(n, 1), dtype=np.uint32)
     _check(lib().neng_debug_libm_eval(device, func, lo, n, out.ctypes.data_as(C.POINTER(C.c_uint32))))
     return out[:n]
+
+
+def solve_decoders(activities: np.ndarray, targets: np.ndarray, reg: float = 0.1) -> np.ndarray:
+    """solve_decoders (frontend.cpp:56-76), native and Eigen-free: the
+    regularised least-squares decoders D [n][d] with
+    (A^T A + m sigma^2 I) D = A^T Y, sigma = reg * max|A|, for activities
+    A [m][n] and targets Y [m][d] (a 1-D Y is one target column)."""
+    a = np.ascontiguousarray(activities, dtype=np.float64)
+    y = np.ascontiguousarray(targets, dtype=np.float64)
+    if y.ndim == 1:
+        y = y[:, None]
+    if a.ndim != 2 or y.ndim != 2 or a.shape[0] != y.shape[0]:
+        raise ValueError("solve_decoders: activities [m][n] and targets [m][d] expected")
+    m, n = a.shape
+    d = y.shape[1]
+    out = np.zeros((n, d))
+    f64 = C.POINTER(C.c_double)
+    _check(lib().neng_solve_decoders(a.ctypes.data_as(f64), m, n, y.ctypes.data_as(f64), d, float(reg),
+                                     out.ctypes.data_as(f64)))
+    return out
