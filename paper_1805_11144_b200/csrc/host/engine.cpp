@@ -22,7 +22,9 @@ namespace nengb {
 
 // kernels (generic.cu)
 cudaError_t launch_generic(const GenericProgram& p, int grid, int k_begin, int k_end, int call_k0,
-                           cudaStream_t stream);
+                           cudaStream_t stream, int64_t small_arena_floats = 0);
+size_t generic_small_arena_limit();
+size_t generic_small_smem_bytes(const GenericProgram& p, int64_t arena_floats);
 int generic_max_coresident_blocks(int device);
 cudaError_t launch_reset(float* arena, const float* pristine, const int64_t* base, const int64_t* pbase,
                          const int64_t* span, const int32_t* per_batch, int nbuf, int B, cudaStream_t stream);
@@ -512,7 +514,14 @@ void Engine::compile_generic() {
                     dm.items = dm.a[1].elems;
                     if (dm.a[0].elems == 1) dm.flags |= MF_SCALAR_A;
                     break;
-                case OpKind::DotInc: dm.items = dm.a[2].elems; break;
+                case OpKind::DotInc: {
+                    dm.items = dm.a[2].elems;
+                    const Signal& As = m.signals[op.operands[0].signal];
+                    if (As.constant && std::all_of(As.initial.begin(), As.initial.end(),
+                                                   [](double v) { return std::isfinite(static_cast<float>(v)); }))
+                        dm.flags |= MF_SKIP_ZERO_X;
+                    break;
+                }
                 case OpKind::SimNeurons: dm.items = dm.a[0].elems; break;
                 case OpKind::SimProcess: dm.items = dm.a[0].elems; break;
                 case OpKind::SimPES:
@@ -645,6 +654,8 @@ void Engine::compile_generic() {
         dst.ensure(std::max<size_t>(bytes, 16));
         if (bytes) cuda_check(cudaMemcpy(dst.p, src, bytes, cudaMemcpyHostToDevice), "program H2D");
     };
+    prof_kinds_.clear();
+    for (const DGroup& g : groups) prof_kinds_.push_back(g.kind | (g.flags << 8));
     upload(d_groups_, groups.data(), groups.size() * sizeof(DGroup));
     upload(d_members_, members.data(), members.size() * sizeof(DMember));
     upload(d_tiles_, tiles.data(), tiles.size() * sizeof(DTile));
@@ -674,6 +685,16 @@ void Engine::compile_generic() {
     grid_ = std::max(1, std::min(maxco, max_tiles));
     // tiny programs: one CTA, block-level barriers only (config 0: 42 vs 60 us/step on 4 CTAs)
     if (max_tiles <= 16 && !std::getenv("NENG_GENERIC_GRID")) grid_ = 1;
+    // ... and when the whole arena fits in shared memory, the arena lives there during a launch
+    small_arena_floats_ = 0;
+    // (dense DotInc tiles are written for exactly kTile threads: those programs keep the plain kernel)
+    const bool any_dense =
+        std::any_of(groups.begin(), groups.end(), [](const DGroup& g) { return (g.flags & GF_DENSE) != 0; });
+    prog_.n_members = static_cast<int32_t>(members.size());
+    prog_.n_tiles = static_cast<int32_t>(tiles.size());
+    if (grid_ == 1 && tc_groups_.empty() && !any_dense && !std::getenv("NENG_GENERIC_NO_SMEM") &&
+        generic_small_smem_bytes(prog_, arena_floats_) <= generic_small_arena_limit())
+        small_arena_floats_ = arena_floats_;
     if (std::getenv("NENG_GENERIC_VERBOSE"))
         std::fprintf(stderr, "[generic] %zu groups, max tiles %d, grid %d\n", groups.size(), max_tiles, grid_);
 }
@@ -787,7 +808,27 @@ void Engine::launch_steps(int n_steps, const float* d_feed_data, const std::vect
     } else {
         int K = steps_per_launch_ > 0 ? steps_per_launch_ : n_steps;
         for (int k = 0; k < n_steps; k += K) {
-            cuda_check(launch_generic(p, grid_, k, std::min(n_steps, k + K), 0, stream), "generic kernel launch");
+            const bool prof = std::getenv("NENG_GENERIC_PROFILE") != nullptr;
+            DevMem dprof;
+            if (prof) {
+                dprof.ensure((prog_.n_groups + 1) * 8);
+                cuda_check(cudaMemsetAsync(dprof.p, 0, (prog_.n_groups + 1) * 8, stream), "profile reset");
+                p.prof = dprof.as<unsigned long long>();
+            }
+            cuda_check(launch_generic(p, grid_, k, std::min(n_steps, k + K), 0, stream, small_arena_floats_),
+                       "generic kernel launch");
+            if (prof) {
+                std::vector<unsigned long long> h(prog_.n_groups);
+                cuda_check(cudaMemcpyAsync(h.data(), dprof.p, h.size() * 8, cudaMemcpyDeviceToHost, stream), "prof");
+                cuda_check(cudaStreamSynchronize(stream), "prof");
+                const int nk = std::min(n_steps, k + K) - k;
+                std::fprintf(stderr, "[generic profile] cycles per step per group (CTA 0):");
+                for (int gi = 0; gi < prog_.n_groups; ++gi)
+                    std::fprintf(stderr, " g%d:%s/f%d=%.0f", gi, op_kind_name(static_cast<OpKind>(prof_kinds_[gi] & 255)),
+                                 prof_kinds_[gi] >> 8, static_cast<double>(h[gi]) / nk);
+                std::fprintf(stderr, "\n");
+                p.prof = nullptr;
+            }
             ++last_launches_;
         }
     }

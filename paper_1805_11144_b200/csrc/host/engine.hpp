@@ -132,6 +132,8 @@ class Engine {
         std::vector<std::unique_ptr<DevMem>> scratch;  // BF16X3 split buffers
     };
     std::vector<TcGroup> tc_groups_;
+    int64_t small_arena_floats_ = 0;
+    std::vector<int32_t> prof_kinds_;  // group kinds (NENG_GENERIC_PROFILE)  // > 0: one CTA runs the interpreter with the arena in shared memory
     void run_tc_dots(const TcGroup& g, cudaStream_t stream);
     int call_steps_ = 0;  // steps of the open stepped call (0: none)
     cudaStream_t call_stream_ = nullptr;

@@ -33,6 +33,14 @@ __device__ __forceinline__ float* at(const GenericProgram& p, const DArg& a, int
 
 // One work item of a data-parallel group. local indexes the member's
 // per-copy work (element, row, or (row, col) for PES).
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+
+/// SMALL: the arena is in shared memory (generic_small_kernel).
+template <bool SMALL = false>
 __device__ __forceinline__ void exec_item(const GenericProgram& p, const DGroup& g, const DMember& m,
                                           int64_t local, int b) {
     switch (g.kind) {
@@ -63,8 +71,35 @@ __device__ __forceinline__ void exec_item(const GenericProgram& p, const DGroup&
             const float* x = at(p, m.a[1], 0, b);
             const int32_t xes = m.a[1].es;
             float acc = 0.0f;
+            if (!SMALL && (m.flags & MF_SKIP_ZERO_X)) {  // x[k] first; A[r,k] only for the nonzero terms
+                {
 #pragma unroll 8
-            for (int64_t k = 0; k < n; ++k) acc = acc + arow[k * aes] * x[k * xes];
+                    for (int64_t k = 0; k < n; ++k) {
+                        const float xk = x[k * xes];
+                        if (xk != 0.0f) acc = acc + arow[k * aes] * xk;
+                    }
+                }
+            } else if constexpr (SMALL) {  // shared-memory loads, issued ahead of the (sequential) sum
+                const uint32_t ar = static_cast<uint32_t>(__cvta_generic_to_shared(arow));
+                const uint32_t xr = static_cast<uint32_t>(__cvta_generic_to_shared(x));
+                const uint32_t as = 4u * static_cast<uint32_t>(aes), xs = 4u * static_cast<uint32_t>(xes);
+                const uint32_t n32 = static_cast<uint32_t>(n);
+                uint32_t k = 0;
+                for (; k + 8 <= n32; k += 8) {
+                    float av[8], xv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        av[u] = lds_f32(ar + (k + u) * as);
+                        xv[u] = lds_f32(xr + (k + u) * xs);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) acc = acc + av[u] * xv[u];
+                }
+                for (; k < n32; ++k) acc = acc + lds_f32(ar + k * as) * lds_f32(xr + k * xs);
+            } else {
+#pragma unroll 8
+                for (int64_t k = 0; k < n; ++k) acc = acc + arow[k * aes] * x[k * xes];
+            }
             float* y = at(p, m.a[2], local, b);
             *y = *y + acc;
             break;
@@ -182,6 +217,37 @@ __device__ void dense_dot_tile(const GenericProgram& p, const DMember& m, int ro
     }
 }
 
+/// One DotInc output row by a whole warp, for a constant all-finite A
+/// (MF_SKIP_ZERO_X): lanes form the products of 32 consecutive k at a time
+/// (each rounded, as the reference's), and the nonzero ones are added to the
+/// running sum in ascending k — the reference's sum without its zero terms,
+/// which change nothing (see MF_SKIP_ZERO_X).  The sequential chain is as long
+/// as the number of spikes instead of the row length.
+__device__ __forceinline__ void warp_dot_sparse(const GenericProgram& p, const DMember& m, int64_t local, int b,
+                                                int lane) {
+    const int64_t n = m.a[1].elems;
+    const float* arow = at(p, m.a[0], local * n, b);
+    const float* x = at(p, m.a[1], 0, b);
+    const int32_t aes = m.a[0].es, xes = m.a[1].es;
+    float acc = 0.0f;
+    for (int64_t k0 = 0; k0 < n; k0 += 32) {
+        const int64_t k = k0 + lane;
+        const float xv = k < n ? x[k * xes] : 0.0f;
+        const bool nz = xv != 0.0f;
+        const float pv = nz ? arow[k * aes] * xv : 0.0f;
+        uint32_t bits = __ballot_sync(0xffffffffu, nz);
+        while (bits) {
+            const int c = __ffs(bits) - 1;
+            bits &= bits - 1u;
+            acc = acc + __shfl_sync(0xffffffffu, pv, c);
+        }
+    }
+    if (lane == 0) {
+        float* y = at(p, m.a[2], local, b);
+        *y = *y + acc;
+    }
+}
+
 // Reference loop order for one member and one copy b (GF_SERIAL_ALL).
 __device__ void exec_member_serial(const GenericProgram& p, const DGroup& g, const DMember& m, int b) {
     switch (g.kind) {
@@ -247,14 +313,18 @@ __device__ __forceinline__ void grid_sync(cg::grid_group& grid) {
         grid.sync();
 }
 
-__global__ void __launch_bounds__(kTile) generic_run_kernel(GenericProgram p, int k_begin, int k_end,
-                                                            int call_k0) {
-    cg::grid_group grid = cg::this_grid();
+/// The step loop of the interpreter.  SMALL: one CTA whose arena is in shared
+/// memory (generic_small_kernel); the plain groups' tiles then run side by
+/// side, one 256-thread slice per tile, instead of one after another.
+template <bool SMALL>
+__device__ __forceinline__ void generic_steps(const GenericProgram& p, cg::grid_group& grid, int k_begin, int k_end,
+                                              int call_k0) {
     const int B = p.batch;
     for (int k = k_begin; k < k_end; ++k) {
         const int ks = k - call_k0;  // step index within this run() call
         // write_feeds (exec.cpp:313-326): per-batch slots take row b, shared slots row 0
         const int g_end = p.g_end < 0 ? p.n_groups : p.g_end;
+        unsigned long long prof_t = p.prof ? clock64() : 0ull;
         if (p.any_feed && p.g_begin == 0) {
             for (int f = 0; f < p.n_feeds; ++f) {
                 const DFeed& fd = p.feeds[f];
@@ -294,18 +364,42 @@ __global__ void __launch_bounds__(kTile) generic_run_kernel(GenericProgram p, in
                     const DTile tl = p.tiles[g.tile_begin + t];
                     dense_dot_tile(p, p.members[tl.member], tl.start, tl.count);
                 }
+            } else if (SMALL && g.n_tiles == 1 && p.tiles[g.tile_begin].count <= 32) {
+                // a few long items (a decoder's 16 sequential 800-term sums): one per warp, lane 0 —
+                // lanes of one warp reading different rows of a row-major matrix at the same
+                // column hit one shared-memory bank; separate warps do not conflict
+                const DTile tl = p.tiles[g.tile_begin];
+                const int j = threadIdx.x >> 5, lane = threadIdx.x & 31;
+                if (j < tl.count) {
+                    const int i = tl.start + j;
+                    const int local = i / g.copies;
+                    const DMember& m = p.members[tl.member];
+                    if (g.kind == 3 && (m.flags & MF_SKIP_ZERO_X))
+                        warp_dot_sparse(p, m, local, i - local * g.copies, lane);
+                    else if (lane == 0)
+                        exec_item<SMALL>(p, g, m, local, i - local * g.copies);
+                }
             } else {
-                for (int t = blockIdx.x; t < g.n_tiles; t += gridDim.x) {
+                const int t0 = SMALL ? threadIdx.x / kTile : blockIdx.x;
+                const int ts = SMALL ? blockDim.x / kTile : gridDim.x;
+                const int j0 = SMALL ? threadIdx.x % kTile : threadIdx.x;
+                const int js = SMALL ? kTile : blockDim.x;
+                for (int t = t0; t < g.n_tiles; t += ts) {
                     const DTile tl = p.tiles[g.tile_begin + t];
                     const DMember& m = p.members[tl.member];
-                    for (int j = threadIdx.x; j < tl.count; j += blockDim.x) {
+                    for (int j = j0; j < tl.count; j += js) {
                         const int i = tl.start + j;  // < 2^30 (engine.cpp)
                         const int local = i / g.copies;
-                        exec_item(p, g, m, local, i - local * g.copies);
+                        exec_item<SMALL>(p, g, m, local, i - local * g.copies);
                     }
                 }
             }
             if (g.flags & GF_BARRIER) grid_sync(grid);
+            if (p.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+                const unsigned long long now = clock64();
+                p.prof[gi] += now - prof_t;
+                prof_t = now;
+            }
         }
         // capture_probes (exec.cpp:328-338): shared probes read copy 0
         if (p.n_probes && g_end == p.n_groups) {
@@ -322,6 +416,53 @@ __global__ void __launch_bounds__(kTile) generic_run_kernel(GenericProgram p, in
             grid_sync(grid);
         }
     }
+}
+
+__global__ void __launch_bounds__(kTile) generic_run_kernel(GenericProgram p, int k_begin, int k_end,
+                                                            int call_k0) {
+    cg::grid_group grid = cg::this_grid();
+    generic_steps<false>(p, grid, k_begin, k_end, call_k0);
+}
+
+constexpr int kSmallThreads = 4 * kTile;
+
+/// Programs whose whole arena fits in shared memory (config 0: one 800-neuron
+/// ensemble, ~170 KB): one CTA copies the arena in, runs the launch's steps on
+/// it (every operand access a shared-memory access instead of an L2 round trip
+/// after the previous group's stores), and copies it back.
+__global__ void __launch_bounds__(kSmallThreads) generic_small_kernel(GenericProgram p, int k_begin, int k_end,
+                                                                      int call_k0, int64_t arena_floats) {
+    // shared: the program's group / member / tile descriptors (copied once: every group's
+    // decode is then a shared-memory read), then the arena
+    extern __shared__ __align__(16) float sarena[];
+    cg::grid_group grid = cg::this_grid();
+    DMember* smem_members = reinterpret_cast<DMember*>(sarena);
+    DGroup* smem_groups = reinterpret_cast<DGroup*>(smem_members + p.n_members);
+    DTile* smem_tiles = reinterpret_cast<DTile*>(smem_groups + p.n_groups);
+    const size_t desc_bytes = (p.n_members * sizeof(DMember) + p.n_groups * sizeof(DGroup) +
+                               p.n_tiles * sizeof(DTile) + 15) & ~size_t{15};
+    float* arena = reinterpret_cast<float*>(reinterpret_cast<char*>(sarena) + desc_bytes);
+    for (int i = threadIdx.x; i < p.n_members; i += blockDim.x) smem_members[i] = p.members[i];
+    for (int i = threadIdx.x; i < p.n_groups; i += blockDim.x) smem_groups[i] = p.groups[i];
+    for (int i = threadIdx.x; i < p.n_tiles; i += blockDim.x) smem_tiles[i] = p.tiles[i];
+    float* garena = p.arena;
+    for (int64_t i = threadIdx.x; i < arena_floats; i += blockDim.x) arena[i] = garena[i];
+    __syncthreads();
+    GenericProgram q = p;
+    q.arena = arena;
+    q.members = smem_members;
+    q.groups = smem_groups;
+    q.tiles = smem_tiles;
+    generic_steps<true>(q, grid, k_begin, k_end, call_k0);
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < arena_floats; i += blockDim.x) garena[i] = arena[i];
+}
+
+/// Shared-memory bytes of the small variant for a program (descriptors + arena).
+size_t generic_small_smem_bytes(const GenericProgram& p, int64_t arena_floats) {
+    const size_t desc = (p.n_members * sizeof(DMember) + p.n_groups * sizeof(DGroup) + p.n_tiles * sizeof(DTile) +
+                         15) & ~size_t{15};
+    return desc + static_cast<size_t>(arena_floats) * sizeof(float);
 }
 
 // reset (exec.cpp:164-174): broadcast the pristine image to every copy
@@ -384,10 +525,26 @@ __global__ void libm_eval_kernel(int func, uint32_t lo, int64_t n, uint32_t* out
 
 // ---- host launchers --------------------------------------------------------
 
+/// Shared memory the small (arena-in-shared-memory) variant can use (next to the
+/// dense tiles' 12.5 KB of static shared memory).
+size_t generic_small_arena_limit() { return 212 * 1024; }
+
 cudaError_t launch_generic(const GenericProgram& p, int grid, int k_begin, int k_end, int call_k0,
-                           cudaStream_t stream) {
+                           cudaStream_t stream, int64_t small_arena_floats) {
     GenericProgram prog = p;
     void* args[] = {&prog, &k_begin, &k_end, &call_k0};
+    if (small_arena_floats > 0) {
+        const size_t bytes = generic_small_smem_bytes(p, small_arena_floats);
+        static size_t attr = 0;
+        if (bytes > attr) {
+            cudaError_t e = cudaFuncSetAttribute(generic_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(bytes));
+            if (e != cudaSuccess) return e;
+            attr = bytes;
+        }
+        generic_small_kernel<<<1, kSmallThreads, bytes, stream>>>(prog, k_begin, k_end, call_k0, small_arena_floats);
+        return cudaGetLastError();
+    }
     if (grid <= 1) {
         generic_run_kernel<<<1, kTile, 0, stream>>>(prog, k_begin, k_end, call_k0);
         return cudaGetLastError();

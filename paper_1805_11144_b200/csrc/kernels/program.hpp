@@ -48,7 +48,10 @@ enum : int32_t {
     GF_DENSE = 64,      // DotInc with shared row-major A, per-batch x and y: CTA tiles (DTile = member, row0, col0)
 };
 
-enum : int32_t { MF_SCALAR_A = 1 };
+// MF_SKIP_ZERO_X: a DotInc whose A is a constant, all-finite signal skips the terms with
+// x[k] == 0 — exact: A[r,k] * (+-0) is +-0 and the running sum, started at +0, is never
+// -0, so adding it changes nothing (spike vectors are mostly zeros)
+enum : int32_t { MF_SCALAR_A = 1, MF_SKIP_ZERO_X = 2 };
 
 struct DMember {
     DArg a[4];
@@ -130,6 +133,7 @@ struct GenericProgram {
     const DFeed* feeds = nullptr;
     const DProbe* probes = nullptr;
     int32_t n_groups = 0, n_feeds = 0, n_probes = 0, batch = 1;
+    int32_t n_members = 0, n_tiles = 0;  // descriptor counts (the shared-memory variant copies them)
     int32_t g_begin = 0, g_end = -1;  // plan groups this launch runs (-1: to the end); feeds with
                                       // the first group, probe captures with the last
     int32_t any_feed = 0;
@@ -138,6 +142,7 @@ struct GenericProgram {
     const float* feed_data = nullptr;
     float* ring = nullptr;
     int32_t call_steps = 0;
+    unsigned long long* prof = nullptr;  // NENG_GENERIC_PROFILE: per group, clock cycles (CTA 0, summed over steps)
 };
 
 }  // namespace nengb
