@@ -653,6 +653,18 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
         bulk_g2s(S.bias, p.values + e.bias_off, bb, S.bar);
         if (pb) bulk_g2s(S.P, p.values + e.dec_scaled_off, pb, S.bar);
     }
+    // L2 prefetch of the unit's first HBM reads (overlapping the dependency wait and the
+    // connection updates): the incoming connections' filter-state rows and the first
+    // kL2Ahead rows of v and r (the sweep prefetches the rest ahead of itself).  Only
+    // when the unit spans every column (the rows are then contiguous).
+    if (warp == 0 && p.groups == 1 && p.tu * 32 >= B && (B & 3) == 0) {
+        if (lane < e.inc_count) {
+            const FConn& cn = p.conns[__ldg(p.incoming + e.inc_begin + lane)];
+            prefetch_l2_bulk(A + cn.state_base, static_cast<uint32_t>(cn.dd * B) * 4u);
+        } else if (lane >= 30) {
+            prefetch_l2_bulk(A + (lane == 30 ? e.v_base : e.r_base), static_cast<uint32_t>(min(kL2Ahead, e.n) * B) * 4u);
+        }
+    }
     if (df_pos >= 0) {  // barrier-free schedule: wait for the dependencies (overlaps the staging copies)
         df_wait(p, ei, g, df_t);
         __syncthreads();
