@@ -256,10 +256,12 @@ int64_t neng_gpu_last_launch_count(const neng_engine* e);
 
 /* Schedules the most recent run / run_device / stepped call used (bit set):
  * the generic interpreter, the fused pipeline with one grid barrier per step,
- * the fused pipeline's barrier-free stepping. */
+ * the fused pipeline's barrier-free stepping, the fused step on one CTA
+ * (programs too small to fill the GPU). */
 #define NENG_SCHED_GENERIC 1
 #define NENG_SCHED_FUSED_STEPPED 2
 #define NENG_SCHED_FUSED_BARRIER_FREE 4
+#define NENG_SCHED_FUSED_SMALL 8
 int32_t neng_gpu_last_schedule(const neng_engine* e);
 
 /* The tensor-core DotInc of the TF32 / BF16X3 precision modes on its own

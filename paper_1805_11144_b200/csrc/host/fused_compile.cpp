@@ -38,6 +38,7 @@ namespace nengb {
 int fused_dmax_for(int d);
 size_t fused_smem_bytes(const FusedProgram& p, int dmax);
 cudaError_t launch_fused(const FusedProgram& p, int dmax, int grid, int k0, int k1, cudaStream_t stream);
+cudaError_t launch_fused_small(const FusedProgram& p, int dmax, int k0, int k1, cudaStream_t stream);
 cudaError_t launch_feed_projection(const FProj* proj, int nproj, const float* weights, const float* feed_data,
                                    const int64_t* feed_off, const int32_t* present, const float* arena, float* out,
                                    int n_steps, int k0, int k1, int B, cudaStream_t stream);
@@ -59,6 +60,7 @@ class FusedImpl : public FusedPlan {
   public:
     FusedProgram prog;
     int dmax = 8, grid = 1, steps_per_launch = 0;
+    bool small = false;  // fused_small_kernel: the whole step on one CTA (programs too small to fill the GPU)
     DevMem d_ens, d_conns, d_incoming, d_orphans, d_my_conns, d_values, d_probes, d_feeds, d_call, d_prof, d_work, d_xbuf, d_df, d_proj, d_projw, d_projout;
     int n_proj = 0, proj_rows = 0;  // fed-node projections (FProj)
     std::vector<FProj> h_proj;
@@ -133,7 +135,8 @@ class FusedImpl : public FusedPlan {
         cuda_check(cudaMemsetAsync(d_work.p, 0, 8, stream), "fused work reset");
         sched |= NENG_SCHED_FUSED_STEPPED;
         project(p, k0, k1, stream);
-        cuda_check(launch_fused(p, dmax, grid, k0, k1, stream), "fused kernel launch");
+        cuda_check(small ? launch_fused_small(p, dmax, k0, k1, stream) : launch_fused(p, dmax, grid, k0, k1, stream),
+                   "fused kernel launch");
         trace_check(stream);
     }
 
@@ -149,9 +152,10 @@ class FusedImpl : public FusedPlan {
         p.dataflow = dataflow ? 1 : 0;
         cuda_check(cudaMemsetAsync(d_work.p, 0, dataflow ? 16 + static_cast<size_t>(units) * 4 : 8, stream),
                    "fused work reset");
-        sched |= dataflow ? NENG_SCHED_FUSED_BARRIER_FREE : NENG_SCHED_FUSED_STEPPED;
+        sched |= small ? NENG_SCHED_FUSED_SMALL : dataflow ? NENG_SCHED_FUSED_BARRIER_FREE : NENG_SCHED_FUSED_STEPPED;
         project(p, k0, k1, stream);
-        cuda_check(launch_fused(p, dmax, grid, k0, k1, stream), "fused kernel launch");
+        cuda_check(small ? launch_fused_small(p, dmax, k0, k1, stream) : launch_fused(p, dmax, grid, k0, k1, stream),
+                   "fused kernel launch");
         trace_check(stream);
     }
 
@@ -613,10 +617,28 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             for (const FEns& x : fe) fan_in = std::max(fan_in, x.inc_count);
             if (fan_in > 64 && eng.requested_mode() == NENG_MODE_AUTO && W == 1)
                 fail("fan-in " + std::to_string(fan_in) + " above 64 (the generic executor is faster)");
-            // a step of fewer than 4 units runs on as many CTAs: the interpreter spreads the
-            // same work over the whole GPU (config 0, one ensemble at B=1: 42 vs 113 us/step)
+            // programs too small to fill the GPU (fewer than 4 units per step, or batch
+            // columns that leave most lanes of a tile idle) run the whole step on one
+            // CTA with lanes over neurons (fused_small_kernel; config 0, one ensemble at
+            // B=1: the multi-CTA pipeline took 113 us/step, the interpreter 29.5)
             const int64_t step_units = static_cast<int64_t>(fe.size()) * ((B + 255) / 256);
-            if (step_units < 4 && eng.requested_mode() == NENG_MODE_AUTO && W == 1)
+            int64_t neuron_cols = 0, words = 0;
+            for (const FEns& x : fe) {
+                neuron_cols += static_cast<int64_t>(x.n) * B;
+                words += static_cast<int64_t>((x.n + 31) / 32) * B;
+            }
+            int64_t pfloats = 0;
+            for (const FEns& x : fe) pfloats += static_cast<int64_t>(x.n) * x.dx;
+            const char* se = std::getenv("NENG_FUSED_SMALL");  // 0: never, 1: whenever it fits
+            int64_t nmax_cols = 0;  // the decode's index lists: (nmax rounded to 32 + 1) x B ints
+            for (const FEns& x : fe) nmax_cols = std::max<int64_t>(nmax_cols, (static_cast<int64_t>(x.n) + 31) / 32 * 32);
+            const int64_t fixed = words + (nmax_cols + 1) * B;
+            const bool fits = W == 1 && fixed * 4 <= 200 * 1024;
+            p.small_pfloats = (fixed + pfloats) * 4 <= 200 * 1024 ? static_cast<int32_t>(pfloats) : 0;
+            impl->small = fits && (se ? std::atoi(se) != 0
+                                      : (step_units < 4 || B < 32) && neuron_cols <= 65536);
+            p.small_words = static_cast<int32_t>(words);
+            if (step_units < 4 && !impl->small && eng.requested_mode() == NENG_MODE_AUTO && W == 1)
                 fail("only " + std::to_string(step_units) + " unit(s) per step (the generic executor is faster)");
         }
         std::vector<FConn> fc;
@@ -870,7 +892,8 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         // barrier-free stepping (unsharded): claim order of the units
         impl->units = (ens_hi - ens_lo) * p.groups;
         const char* dfe = std::getenv("NENG_FUSED_DATAFLOW");
-        impl->dataflow = W == 1 && !(dfe && std::atoi(dfe) == 0);
+        impl->dataflow = W == 1 && !(dfe && std::atoi(dfe) == 0) && !impl->small;
+        if (impl->small) impl->grid = 1;
         {
             const int NE = static_cast<int>(fe.size());
             const int window = (impl->grid + p.groups - 1) / p.groups;  // ensembles in flight at once
@@ -903,7 +926,8 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         std::ostringstream os;
         os << "fused: " << p.n_ens << " ensembles, " << p.n_conn << " connections, dmax " << impl->dmax << ", grid "
            << impl->grid << ", tiles/unit " << p.tu << ", slices " << p.slices << ", stage_dec " << p.stage_dec
-           << ", smem " << fused_smem_bytes(p, impl->dmax) << (impl->dataflow ? ", barrier-free" : "");
+           << ", smem " << fused_smem_bytes(p, impl->dmax) << (impl->dataflow ? ", barrier-free" : "")
+           << (impl->small ? ", small (one CTA, lanes over neurons)" : "");
         impl->desc = os.str();
         return impl;
     } catch (const Fail& f) {

@@ -1136,6 +1136,212 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fused_run_kernel(const _
     tk.flush(p.prof);
 }
 
+// ---- the small-program step ---------------------------------------------------
+
+constexpr int kSmallThreads = 512;
+
+/// Programs too small to fill the GPU (config 0: one 800-neuron ensemble at
+/// batch 1) run on ONE CTA, phase by phase with block barriers, and with lanes
+/// over (ensemble, neuron, column) items instead of batch columns: the step's
+/// dependency chain, not the GPU's width, is the cost.  Per step k:
+///   deferred work of step k-1 (destination-less connections, captures, clock);
+///   connection updates of step k-1 into every ensemble, one (connection, row,
+///   column) per item (conn_rows: the sequential T.src sum and lowpass_step);
+///   input sums in plan order (Copy increments, exec.cpp:189-210) into the arena;
+///   the neuron sweep (DotInc(E, in, J) sequential in j, lif_spike_step<float>
+///   with glibc's expm1f / log1pf), spike bits into shared-memory words;
+///   the decode, one (ensemble, row, column) per item: payload + the spiking
+///   neurons' products fp32(D[r,i]) * fp32(amp/dt) in ascending i.
+/// Every sum keeps the reference's order, so results are the fused kernel's
+/// (and EngineCore<float>'s) bit for bit.
+/// Step-kk updates of the connections list[0, nc), one (connection, row, column) per item.
+template <int DMAX>
+__device__ void small_conn_rows(const FusedProgram& p, int kk, const int* list, int nc, bool last) {
+    const int B = p.batch;
+    const int64_t items = static_cast<int64_t>(nc) * DMAX * B;
+    for (int64_t it = threadIdx.x; it < items; it += blockDim.x) {
+        const int q = static_cast<int>(it / (DMAX * B));
+        const int r = static_cast<int>((it / B) % DMAX), b = static_cast<int>(it % B);
+        const FConn& cn = p.conns[__ldg(list + q)];
+        if (r >= cn.dd) continue;
+        float f[DMAX];
+        conn_rows<DMAX, 0>(p, cn, kk, b, r, r + 1, true, last, f);
+    }
+}
+
+template <int DMAX>
+__global__ void __launch_bounds__(kSmallThreads) fused_small_kernel(const __grid_constant__ FusedProgram p, int k_begin,
+                                                                     int k_end) {
+    extern __shared__ uint32_t swords[];
+    const int B = p.batch;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    float* A = p.arena;
+    // the decoder products of every ensemble, staged once per launch when they fit
+    // (p.small_pfloats > 0; ensembles in order, each n*dx floats from dec_scaled_off)
+    float* sP = reinterpret_cast<float*>(swords + p.small_words);
+    int* scnt = reinterpret_cast<int*>(sP + p.small_pfloats);  // [B] spike counts (decode)
+    int* sidx = scnt + B;                                      // [B][nmax] spiking neurons (decode)
+    if (p.small_pfloats > 0) {
+        int at = 0;
+        for (int ei = 0; ei < p.n_ens; ++ei) {
+            const int n = p.ens[ei].n * p.ens[ei].dx;
+            const float* src = p.values + p.ens[ei].dec_scaled_off;
+            for (int q = tid; q < n; q += nt) sP[at + q] = __ldg(src + q);
+            at += n;
+        }
+        __syncthreads();
+    }
+    unsigned long long t0 = 0, sec[FS_COUNT] = {};  // NENG_FUSED_PROFILE: ns per phase (thread 0)
+    auto tick = [&](int s) {
+        if (p.prof && tid == 0) {
+            const unsigned long long t = gtime();
+            if (t0) sec[s] += t - t0;
+            t0 = t;
+        }
+    };
+    tick(FS_EPI);
+    for (int k = k_begin; k < k_end; ++k) {
+        const bool last = k == p.call_steps - 1;
+        const bool upd = k > k_begin || p.first_update;
+        if (last) write_feeds<0>(p, k, tid, nt);
+        if (upd) {  // step k-1's destination-less connections (row-parallel), captures and clock
+            small_conn_rows<DMAX>(p, k - 1, p.orphans, p.n_orphans, false);
+            step_work<DMAX, 0>(p, k - 1, nullptr, 0, 1, false, tid, nt);
+        }
+        for (int w = tid; w < p.small_words; w += nt) swords[w] = 0u;
+        __syncthreads();
+        tick(FS_DEFER);
+        if (upd) {  // connection updates of step k-1 into the ensembles
+            small_conn_rows<DMAX>(p, k - 1, p.dest_conns, p.n_dest_conns, false);
+            __syncthreads();
+        }
+        for (int ei = 0; ei < p.n_ens; ++ei) {  // input sums: payload, then the filtered values in plan order
+            const FEns& e = p.ens[ei];
+            for (int it = tid; it < e.d * B; it += nt) {
+                const int r = it / B, b = it - (it / B) * B;
+                float in = __ldg(p.values + e.in_init_off + r);
+                for (int q = 0; q < e.inc_count; ++q) {
+                    const FConn& cn = p.conns[__ldg(p.incoming + e.inc_begin + q)];
+                    in = in + A[cn.state_base + static_cast<int64_t>(r) * B + b];
+                }
+                A[e.in_base + static_cast<int64_t>(r) * B + b] = in;
+            }
+        }
+        __syncthreads();
+        tick(FS_IN);
+        int wofs = 0;
+        for (int ei = 0; ei < p.n_ens; ++ei) {  // the neuron sweep
+            const FEns e = p.ens[ei];  // a private copy: fields stay in registers across the arena stores
+            const int nw = (e.n + 31) >> 5;
+            const float* E = p.values + e.epad_off;
+            for (int it = tid; it < e.n * B; it += nt) {
+                const int i = it / B, b = it - (it / B) * B;
+                float x[DMAX], w[DMAX];
+#pragma unroll
+                for (int j = 0; j < DMAX; ++j) {
+                    x[j] = j < e.d ? A[e.in_base + static_cast<int64_t>(j) * B + b] : 0.0f;
+                    w[j] = j < e.d ? __ldg(E + (i >> 1) * 2 * DMAX + j * 2 + (i & 1)) : 0.0f;
+                }
+                float acc = 0.0f;
+#pragma unroll
+                for (int j = 0; j < DMAX; ++j)
+                    if (j < e.d) acc = acc + w[j] * x[j];
+                const float J = __ldg(p.values + e.bias_off + i) + acc;
+                const int64_t o = static_cast<int64_t>(i) * B + b;
+                float v = A[e.v_base + o], r = A[e.r_base + o];
+                const bool spike = lif_step(J, v, r, e.dt, e.em_dt, e.inv_tau_rc, e.tau_rc, e.tau_ref,
+                                            [&](float a, bool is_log) { return glibc_value(a, is_log, p); });
+                A[e.v_base + o] = v;
+                A[e.r_base + o] = r;
+                if (spike) atomicOr(swords + wofs + b * nw + (i >> 5), 1u << (i & 31));
+                if (last) {
+                    A[e.j_base + o] = J;
+                    A[e.out_base + o] = spike ? e.amp_dt : 0.0f;
+                }
+                for (int c = 0; c < e.sc_count; ++c) {  // captures of the ensemble's own neuron signals
+                    const int2 cap = __ldg(reinterpret_cast<const int2*>(p.scaps) + e.sc_begin + c);
+                    const float val = cap.x == SC_OUT ? (spike ? e.amp_dt : 0.0f)
+                                      : cap.x == SC_VOLTAGE ? v
+                                      : cap.x == SC_REFRACTORY ? r
+                                                               : J;
+                    p.ring[p.ring_off[cap.y] + static_cast<int64_t>(k) * e.n * B + o] = val;
+                }
+            }
+            wofs += nw * B;
+        }
+        __syncthreads();
+        tick(FS_SWEEP);
+        wofs = 0;
+        int pofs = 0;
+        for (int ei = 0; ei < p.n_ens; ++ei) {  // the decode
+            const FEns e = p.ens[ei];
+            const int nw = (e.n + 31) >> 5;
+            const float* P = p.small_pfloats > 0 ? sP + pofs : p.values + e.dec_scaled_off;
+            pofs += e.n * e.dx;
+            // 1. the spiking neurons of every column, ascending, compacted into sidx[b][0, cnt_b)
+            //    (a thread per (word, column): its rank is the popcount of the words before)
+            for (int it = tid; it < nw * B; it += nt) {
+                const int b = it / nw, w = it - b * nw;
+                const uint32_t* cw = swords + wofs + b * nw;
+                int pos = 0;
+                for (int q = 0; q < w; ++q) pos += __popc(cw[q]);
+                uint32_t bits = cw[w];
+                int* out = sidx + b * e.n;
+                if (w == nw - 1) scnt[b] = pos + __popc(bits);
+                while (bits) {
+                    out[pos++] = w * 32 + __ffs(bits) - 1;
+                    bits &= bits - 1u;
+                }
+            }
+            __syncthreads();
+            // 2. a thread per (row, column): payload + the products of those neurons in order,
+            //    eight indices and eight products in flight ahead of the dependent adds
+            for (int it = tid; it < e.dx * B; it += nt) {
+                const int r = it / B, b = it - (it / B) * B;
+                const int cnt = scnt[b];
+                const int* ix = sidx + b * e.n;
+                const float* Pr = P + r;
+                float a = 0.0f;
+                int q = 0;
+                for (; q + 8 <= cnt; q += 8) {
+                    float t[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) t[u] = Pr[ix[q + u] * e.dx];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) a = a + t[u];
+                }
+                for (; q < cnt; ++q) a = a + Pr[ix[q] * e.dx];
+                const float xv = __ldg(p.values + e.xhat_init_off + r) + a;
+                p.xbuf[(xslot(p, k) * p.xrows + e.xb_row + r) * B + b] = xv;
+                if (last) A[e.xhat_base + static_cast<int64_t>(r) * B + b] = xv;
+            }
+            __syncthreads();  // sidx / scnt are reused by the next ensemble
+            wofs += nw * B;
+        }
+        __syncthreads();
+        tick(FS_DECODE);
+    }
+    if (p.epilogue) {  // connection updates, captures and clock of the launch's last step
+        small_conn_rows<DMAX>(p, k_end - 1, p.my_conns, p.n_my_conns, k_end - 1 == p.call_steps - 1);
+        step_work<DMAX, 0>(p, k_end - 1, nullptr, 0, 1, k_end - 1 == p.call_steps - 1, tid, nt);
+    }
+    tick(FS_EPI);
+    if (p.prof && tid == 0)
+        for (int s2 = 0; s2 < FS_COUNT; ++s2) atomicAdd(p.prof + s2, sec[s2]);
+}
+
+template <int DMAX>
+cudaError_t launch_small(const FusedProgram& p, int k0, int k1, cudaStream_t stream) {
+    const size_t sm = (static_cast<size_t>(p.small_words) + p.small_pfloats + p.batch + static_cast<size_t>(p.nmax) * p.batch) * 4;
+    if (sm > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(fused_small_kernel<DMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(sm));
+        if (e != cudaSuccess) return e;
+    }
+    fused_small_kernel<DMAX><<<1, kSmallThreads, sm, stream>>>(p, k0, k1);
+    return cudaGetLastError();
+}
+
 template <int DMAX, int BT, bool PROF, bool DF>
 cudaError_t launch_k(const FusedProgram& p, int grid, int k0, int k1, cudaStream_t stream) {
     size_t sm = smem_bytes<DMAX>(p);
@@ -1224,6 +1430,19 @@ cudaError_t launch_fused(const FusedProgram& p, int dmax, int grid, int k0, int 
         case 8: return prof ? launch_d<8, true>(p, grid, k0, k1, stream) : launch_d<8, false>(p, grid, k0, k1, stream);
         case 16: return prof ? launch_d<16, true>(p, grid, k0, k1, stream) : launch_d<16, false>(p, grid, k0, k1, stream);
         case 32: return prof ? launch_d<32, true>(p, grid, k0, k1, stream) : launch_d<32, false>(p, grid, k0, k1, stream);
+#endif
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_fused_small(const FusedProgram& p, int dmax, int k0, int k1, cudaStream_t stream) {
+    FusedProgram q = p;
+    q.dataflow = 0;  // parity xhat slots: the step's phases are ordered by block barriers
+    switch (dmax) {
+        case 8: return launch_small<8>(q, k0, k1, stream);
+#ifndef NENG_FUSED_DEBUG_BUILD
+        case 16: return launch_small<16>(q, k0, k1, stream);
+        case 32: return launch_small<32>(q, k0, k1, stream);
 #endif
     }
     return cudaErrorInvalidValue;

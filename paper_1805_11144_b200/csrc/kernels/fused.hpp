@@ -105,6 +105,8 @@ struct FusedProgram {
     int32_t tu = 8, slices = 1, groups = 1;  // tiles per unit, warps per tile, units per ensemble
     int32_t has_time = 0, time_probe_step = -1, time_probe_time = -1;
     int32_t stage_dec = 0;    // decoder products staged into shared memory (when they fit)
+    int32_t small_words = 0;  // fused_small_kernel: spike words, sum over ensembles of B * ceil(n / 32)
+    int32_t small_pfloats = 0;  // fused_small_kernel: decoder products staged in shared memory (sum n*dx), or 0
     int32_t pmax_floats = 0;  // max over ensembles of n*dx rounded up to 4
     int64_t step_base = 0, time_base = 0;
     float dt = 0.f;

@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libneng_gpu.so")
 MODE_AUTO, MODE_GENERIC, MODE_FUSED = 0, 1, 2
 PRECISION_STRICT_FP32, PRECISION_TF32, PRECISION_BF16X3 = 0, 1, 2
 STEP_FIRST_UPDATE, STEP_EPILOGUE = 1, 2
-SCHED_GENERIC, SCHED_FUSED_STEPPED, SCHED_BARRIER_FREE = 1, 2, 4  # neng_gpu_last_schedule bits
+SCHED_GENERIC, SCHED_FUSED_STEPPED, SCHED_BARRIER_FREE, SCHED_FUSED_SMALL = 1, 2, 4, 8  # neng_gpu_last_schedule bits
 
 _lib = None
 

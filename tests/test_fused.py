@@ -14,6 +14,13 @@ from tests.support.models import assert_bitexact, batch_slice, step_slice
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def multi_cta_pipeline(monkeypatch):
+    # these tests cover the multi-CTA fused kernel; tests/test_fused_small.py runs the
+    # one-CTA step that AUTO picks for programs too small to fill the GPU
+    monkeypatch.setenv("NENG_FUSED_SMALL", "0")
+
+
 def full_state_equal(gpu, ref, model, batch, context):
     for s in model.signals:
         for b in {0, batch - 1}:
