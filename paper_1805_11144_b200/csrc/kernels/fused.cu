@@ -461,6 +461,7 @@ __device__ __forceinline__ void conn_rows(const FusedProgram& p, const FConn& cn
 #pragma unroll
     for (int r = 0; r < DMAX; ++r) s0[r] = (valid && r >= r_lo && r < r_hi) ? st[static_cast<int64_t>(r) * B] : 0.0f;
     const float4* Tm = reinterpret_cast<const float4*>(p.values + cn.tpad_off);
+    const bool extra = last || cn.probe_filt >= 0 || cn.probe_state >= 0;
 #pragma unroll
     for (int r = 0; r < DMAX; ++r) {
         if (r < r_lo || r >= r_hi) continue;
@@ -476,8 +477,8 @@ __device__ __forceinline__ void conn_rows(const FusedProgram& p, const FConn& cn
         const float accv = __ldg(p.values + cn.acc_init_off + r) + acc;
         const float f = cn.a * s0[r] + cn.b * accv;  // lowpass_step (neuron_math.hpp:39-42)
         f_out[r] = f;
-        if (valid) {
-            st[static_cast<int64_t>(r) * B] = f;
+        if (valid) st[static_cast<int64_t>(r) * B] = f;
+        if (valid && extra) {  // the call's last step, probe captures (uniform: one branch per row)
             if (last) {
                 A[cn.acc_base + static_cast<int64_t>(r) * B + b] = accv;
                 A[cn.filt_base + static_cast<int64_t>(r) * B + b] = f;
