@@ -133,7 +133,7 @@ class FusedImpl : public FusedPlan {
         p.first_update = (flags & NENG_STEP_FIRST_UPDATE) ? 1 : 0;
         p.epilogue = (flags & NENG_STEP_EPILOGUE) ? 1 : 0;
         cuda_check(cudaMemsetAsync(d_work.p, 0, 8, stream), "fused work reset");
-        sched |= NENG_SCHED_FUSED_STEPPED;
+        sched |= small ? NENG_SCHED_FUSED_SMALL : NENG_SCHED_FUSED_STEPPED;
         project(p, k0, k1, stream);
         cuda_check(small ? launch_fused_small(p, dmax, k0, k1, stream) : launch_fused(p, dmax, grid, k0, k1, stream),
                    "fused kernel launch");

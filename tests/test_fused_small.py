@@ -85,3 +85,50 @@ def test_neuron_state_probes(monkeypatch):
     assert_bitexact(out, ref.run(w.steps, w.feeds), "state probes")
     assert np.count_nonzero(out[pm.model.probes[-4].key]) > 0
     full_state_equal(gpu, ref, pm.model, w.batch, "state probes")
+
+
+def test_wide_fed_connections_projected(monkeypatch):
+    # fed-node connections wider than the fused rows are projected ahead of each launch
+    # (FProj) and read through an identity transform; a second call takes the defaults
+    monkeypatch.setenv("NENG_FUSED_SMALL", "1")
+    w = networks.config1(steps=25, batch=3, dims=40)
+    pm = passes.run_passes(w.model)
+    gpu = GpuEngine(pm, w.batch, mode=MODE_FUSED)
+    ref = refapi.RefEngine(pm, w.batch)
+    assert_bitexact(gpu.run(w.steps, w.feeds), ref.run(w.steps, w.feeds), "projected feeds")
+    assert gpu.last_schedule() == SCHED_FUSED_SMALL
+    full_state_equal(gpu, ref, pm.model, w.batch, "projected feeds")
+    assert_bitexact(gpu.run(7), ref.run(7), "default node values")
+    full_state_equal(gpu, ref, pm.model, w.batch, "default node values")
+
+
+def test_stepped_calls_match_run_device(monkeypatch):
+    # the stepped call (begin / step k / epilogue / end) on the one-CTA step leaves the
+    # same probe ring as one run_device call
+    monkeypatch.setenv("NENG_FUSED_SMALL", "1")
+    import torch
+    from paper_1805_11144_b200.engine import STEP_EPILOGUE, STEP_FIRST_UPDATE
+    from tests.support.device import device_feeds, device_ring
+    dev = torch.device("cuda", 0)
+    w = small_network(seed=2, batch=2, steps=12)
+    pm = passes.run_passes(w.model)
+    n, B = w.steps, w.batch
+    ts = torch.cuda.Stream(dev)
+    with torch.cuda.stream(ts):
+        feeds, fptrs = device_feeds(w, n, dev)
+        whole = GpuEngine(pm, B)
+        ring_w, rptrs_w, _ = device_ring(pm.model, n, B, dev)
+        whole.run_device(n, fptrs, rptrs_w, ts.cuda_stream)
+        stepped = GpuEngine(pm, B)
+        ring_s, rptrs_s, _ = device_ring(pm.model, n, B, dev)
+        stepped.call_begin(n, fptrs, rptrs_s, ts.cuda_stream)
+        for k in range(n):
+            stepped.call_step(k, STEP_FIRST_UPDATE if k else 0)
+        stepped.call_step(n, STEP_EPILOGUE)
+        stepped.call_end()
+        torch.cuda.synchronize(dev)
+    assert stepped.last_schedule() & SCHED_FUSED_SMALL
+    assert torch.equal(ring_w.view(torch.int32), ring_s.view(torch.int32))
+    ref = refapi.RefEngine(pm, B)
+    ref.run(n, w.feeds)
+    full_state_equal(stepped, ref, pm.model, B, "stepped")
