@@ -92,6 +92,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+/// ld.shared.f32 at a 32-bit shared-window address (no generic-to-shared conversion).
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -216,6 +222,11 @@ struct Smem {
 };
 
 constexpr int kRingFloats = 2 * 2 * kUnroll * 32;  // per warp
+// The rings of the CTA's warps are interleaved: row `row` of stage `st` of array
+// `arr` (v = 0, r = 1) is line (arr * 2 + st) * kUnroll + row of kRowB bytes,
+// warp w's 32 columns at w * 128; a lane's address is then base + threadIdx.x * 4
+// plus a row offset (nothing warp-dependent to keep live across the sweep).
+constexpr uint32_t kRowB = kWarps * 32 * 4;
 constexpr size_t kQueueBytes = 2 * sizeof(QEnt) * kQ * kWarps;
 
 /// Bytes of the region shared by the input staging `in` and the queues.
@@ -745,30 +756,29 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
         const float2 dt2 = make_float2(dt, dt), ndt2 = make_float2(-dt, -dt);
         // addresses inside the sweep derive from vst (row i, this lane's column): a
         // separate row-0 pointer would be one more 64-bit value live across the loop
-        float* ring = S.ring + warp * kRingFloats;
+        const uint32_t ring_base = smem_addr(S.ring);
         const bool vec = (B & 3) == 0;
         float* vst = A + e.v_base + b0 + static_cast<int64_t>(n0) * B + lane;  // row i of this lane
         const int64_t rdelta = e.r_base - e.v_base;
         // the lane's share of the ring copies (addresses recomputed per round: fewer live
         // registers).  vec (B % 4 == 0): 16 B, columns lc..lc+3 of row lr of each 4-row
         // round; else 4 B (its own column) of every row
-        const uint32_t ring_s = smem_addr(ring);
         auto ring_issue = [&](int st, int r0, const float* rowp) {  // rowp: row r0, this lane's column
             const int lr = vec ? (lane >> 3) : 0, lc = vec ? (lane & 7) * 4 : lane;
             if (b0 + lc < B) {
                 const float* src = rowp + static_cast<int64_t>(lr) * B + (lc - lane);
-                const uint32_t dst = ring_s + (st * kUnroll * 32 + lr * 32 + lc) * 4;
+                const uint32_t dst = ring_base + (st * kUnroll + lr) * kRowB + warp * 128 + lc * 4;
                 if (vec) {
                     if (r0 + lr < n1) {
                         cp_async16_s(dst, src);
-                        cp_async16_s(dst + 2 * kUnroll * 32 * 4, src + rdelta);
+                        cp_async16_s(dst + 2 * kUnroll * kRowB, src + rdelta);
                     }
                 } else {
 #pragma unroll
                     for (int rr = 0; rr < kUnroll; ++rr)
                         if (r0 + rr < n1) {
-                            cp_async4_s(dst + rr * 32 * 4, src + static_cast<int64_t>(rr) * B);
-                            cp_async4_s(dst + rr * 32 * 4 + 2 * kUnroll * 32 * 4, src + static_cast<int64_t>(rr) * B + rdelta);
+                            cp_async4_s(dst + rr * kRowB, src + static_cast<int64_t>(rr) * B);
+                            cp_async4_s(dst + rr * kRowB + 2 * kUnroll * kRowB, src + static_cast<int64_t>(rr) * B + rdelta);
                         }
                 }
             }
@@ -785,7 +795,7 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
         QEnt* qe = S.qe + warp * kQ;  // exceptions: leaving the refractory period (expm1f) or spiking (log1pf)
         QEnt* qd = S.qs + warp * kQ;  // doubtful speculative values: recomputed exactly
         int ne = 0, nd = 0;           // warp-uniform counts
-        const float* ring_l = ring + lane;
+        const uint32_t ring_a = ring_base + threadIdx.x * 4u;  // this lane's column of the ring
         const float* sE = S.E + n0 * DMAX;
         const float* sbias = S.bias + n0;
         for (int i = n0; i < n1; i += 2, vst += 2 * B, sE += 2 * DMAX, sbias += 2) {
@@ -822,10 +832,10 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
                     }
                 }
             }
-            const float* sv = ring_l + (rel & (2 * kUnroll - 1)) * 32;
+            const uint32_t sv = ring_a + static_cast<uint32_t>(rel & (2 * kUnroll - 1)) * kRowB;
             FTRACE(6, i);
-            const float2 v2 = make_float2(sv[0], sv[32]);
-            const float2 r2 = make_float2(sv[2 * kUnroll * 32], sv[2 * kUnroll * 32 + 32]);
+            const float2 v2 = make_float2(lds_f32(sv), lds_f32(sv + kRowB));
+            const float2 r2 = make_float2(lds_f32(sv + 2 * kUnroll * kRowB), lds_f32(sv + 2 * kUnroll * kRowB + kRowB));
             // DotInc(E, in, J) for neurons i, i+1: acc from +0, j ascending, then J = bias + acc;
             // the two neurons' sums side by side (encoders pair-interleaved: [j][i, i+1])
             float acc[2];
