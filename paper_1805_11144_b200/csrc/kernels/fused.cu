@@ -637,6 +637,79 @@ __device__ void df_orphans(const FusedProgram& p, int ei, int g, int k, bool las
     }
 }
 
+/// The decode of one-tile units (B <= 32: the 8 warps are neuron slices of one
+/// tile) whose decoder products were staged separately: the slices compact each
+/// column's spiking neurons into an ascending index list (in the encoder region,
+/// free after the sweep), then every warp chains its own rows over the lists — all
+/// 8 warps decode instead of 2.  Out of line (once per unit): its registers stay out
+/// of the sweep's allocation.  Returns false (nothing written) when a column's list
+/// would not fit; the caller then runs the row-split decode.
+template <int DMAX, int BT>
+__device__ __noinline__ bool decode_listed(const FusedProgram& p, int ei, int k, bool last, float* ring, float* Ebuf,
+                                           const float* P, const uint32_t* words, int slice, bool valid, int b) {
+    const FEns& e = p.ens[ei];
+    const int B = batch_of<BT>(p);
+    const int lane = threadIdx.x & 31;
+    float* A = p.arena;
+    const int nw = (e.n + 31) >> 5;
+    const int cap = static_cast<int>(static_cast<size_t>(p.nmax) * DMAX * 4 / (32 * 2));  // uint16 per column
+    uint16_t* cntw = reinterpret_cast<uint16_t*>(ring);       // [word][column] spike counts (ring: free)
+    int* stot = reinterpret_cast<int*>(ring) + nw * 16;       // [column] list lengths
+    uint16_t* list = reinterpret_cast<uint16_t*>(Ebuf);       // [position][column] (columns interleaved)
+    for (int w = slice; w < nw; w += kWarps) {
+        const int i = w * 32 + lane;
+        uint32_t bits = transpose32(i < e.n ? words[i] : 0u, lane);
+        if (!valid) bits = 0u;
+        cntw[w * 32 + lane] = static_cast<uint16_t>(__popc(bits));
+    }
+    __syncthreads();
+    int tot = 0;
+    for (int w = 0; w < nw; ++w) tot += cntw[w * 32 + lane];
+    if (__any_sync(kFull, tot > cap)) return false;  // the same in every warp: CTA-uniform
+    if (slice == 0) stot[lane] = tot;
+    for (int w = slice; w < nw; w += kWarps) {
+        int pos = 0;
+        for (int q = 0; q < w; ++q) pos += cntw[q * 32 + lane];
+        const int i = w * 32 + lane;
+        uint32_t bits = transpose32(i < e.n ? words[i] : 0u, lane);
+        if (!valid) bits = 0u;
+        while (bits) {
+            list[pos++ * 32 + lane] = static_cast<uint16_t>(w * 32 + __ffs(bits) - 1);
+            bits &= bits - 1u;
+        }
+    }
+    __syncthreads();
+    // a thread per (column, row): the rows of one column sit in consecutive lanes, so the
+    // products P[i][r] of one neuron are consecutive words (no bank conflicts)
+    const int dx = e.dx;
+    for (int it = threadIdx.x; it < 32 * dx; it += blockDim.x) {
+        const int col = it / dx, r = it - col * dx;
+        const int n = stot[col];
+        const uint16_t* lc = list + col;
+        float acc = 0.0f;
+        int q = 0;
+        for (; q + 8 <= n; q += 8) {
+            float t[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t[u] = P[static_cast<int>(lc[(q + u) * 32]) * dx + r];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = acc + t[u];
+        }
+        for (; q < n; ++q) acc = acc + P[static_cast<int>(lc[q * 32]) * dx + r];
+        const int bc = b - lane + col;  // this tile's column col
+        if ((BT > 0 && BT % 32 == 0) || bc < B) {
+            const float xv = __ldg(p.values + e.xhat_init_off + r) + acc;
+            p.xbuf[(xslot(p, k) * p.xrows + e.xb_row + r) * B + bc] = xv;
+            if (last) A[e.xhat_base + static_cast<int64_t>(r) * B + bc] = xv;
+            for (int c = 0; p.dataflow && c < e.xp_count; ++c) {  // barrier-free xhat captures
+                const FProbe& pr = p.probes[__ldg(p.xprobes + e.xp_begin + c)];
+                p.ring[p.ring_off[pr.index] + (static_cast<int64_t>(k) * pr.dim + r) * B + bc] = xv;
+            }
+        }
+    }
+    return true;
+}
+
 template <int DMAX, int BT, bool PROF>
 __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bool last, const Smem& S,
                          uint32_t parity, Ticker<PROF>& tk, int df_pos, int df_t) {
@@ -982,7 +1055,13 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
 
     // 3. decode: rows [r0, r0 + R) of this warp's tile over all neurons, ascending
     FTRACE(13, 0);
-    if (active) {
+    // One-tile units (B <= 32: the 8 warps are neuron slices of one tile) whose decoder
+    // products were staged separately: the slices compact each column's spiking neurons
+    // into an ascending index list (in the encoder region, free after the sweep), then
+    // every warp chains its own rows over the lists — all 8 warps decode instead of 2
+    const bool listed = active && p.tu == 1 && p.slices == kWarps && p.stage_dec &&
+                        decode_listed<DMAX, BT>(p, ei, k, last, S.ring, S.E, S.P, words, slice, valid, b);
+    if (active && !listed) {
         const int dx = e.dx;
         int R = (dx + p.slices - 1) / p.slices;
         if ((dx & 3) == 0) R = (R + 3) & ~3;
@@ -1042,10 +1121,13 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
                 }
             }
         }
-        // out = amp/dt on a spike (the call's last step only reaches the arena)
-        if (last && valid)
-            for (int i = n0; i < n1; ++i)
-                A[e.out_base + static_cast<int64_t>(i) * B + b] = (words[i] >> lane) & 1u ? e.amp_dt : 0.0f;
+    }
+    // out = amp/dt on a spike (the call's last step only reaches the arena)
+    if (active && last && valid) {
+        const int nper = ((e.n + p.slices - 1) / p.slices + 31) & ~31;
+        const int n0 = min(e.n, slice * nper), n1 = min(e.n, n0 + nper);
+        for (int i = n0; i < n1; ++i)
+            A[e.out_base + static_cast<int64_t>(i) * B + b] = (words[i] >> lane) & 1u ? e.amp_dt : 0.0f;
     }
     tk.tick(FS_DECODE);
     FTRACE(14, 0);
