@@ -862,15 +862,17 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
             p.slices = 8 / tu;
             p.groups = (p.btiles + tu - 1) / tu;
         }
-        // stage the decoder products with the encoders when shared memory
-        // allows; prefer a footprint with two CTAs per SM
+        // stage the decoder products with the encoders (else they replace the encoders
+        // after the sweep) when that keeps as many CTAs per SM (at most 3: the register
+        // budget); config 2's 1024-neuron ensembles: 2 CTAs/SM late vs 1 staged, +17%
         {
-            constexpr size_t two = 75 * 1024, one = 227 * 1024;  // "two": the multi-CTA-per-SM budget (3 CTAs)
+            auto per_sm = [](size_t b) { return std::min<size_t>(3, (228 * 1024) / (b + 1024)); };
             p.stage_dec = 1;
             const size_t with = fused_smem_bytes(p, DMAX);
             p.stage_dec = 0;
             const size_t without = fused_smem_bytes(p, DMAX);
-            p.stage_dec = (with <= two || (without > two && with <= one)) ? 1 : 0;
+            p.stage_dec = (with <= 227 * 1024 && per_sm(with) >= per_sm(without)) ? 1 : 0;
+            if (const char* env = std::getenv("NENG_FUSED_STAGE_DEC")) p.stage_dec = std::atoi(env) ? 1 : 0;  // experiments
         }
         p.dt = dt;
         if (time_op >= 0) {

@@ -638,24 +638,25 @@ __device__ void df_orphans(const FusedProgram& p, int ei, int g, int k, bool las
 }
 
 /// The decode of one-tile units (B <= 32: the 8 warps are neuron slices of one
-/// tile) whose decoder products were staged separately: the slices compact each
-/// column's spiking neurons into an ascending index list (in the encoder region,
-/// free after the sweep), then every warp chains its own rows over the lists — all
-/// 8 warps decode instead of 2.  Out of line (once per unit): its registers stay out
+/// tile): the slices compact each column's spiking neurons into an ascending index
+/// list (in the ring and queue regions, free after the sweep), then a thread per
+/// (column, row) chains the products over its column's list — all 8 warps decode
+/// instead of 2, and the sum keeps the ascending neuron order.  Out of line (once per unit): its registers stay out
 /// of the sweep's allocation.  Returns false (nothing written) when a column's list
 /// would not fit; the caller then runs the row-split decode.
 template <int DMAX, int BT>
-__device__ __noinline__ bool decode_listed(const FusedProgram& p, int ei, int k, bool last, float* ring, float* Ebuf,
+__device__ __noinline__ bool decode_listed(const FusedProgram& p, int ei, int k, bool last, float* ring, int lbytes,
                                            const float* P, const uint32_t* words, int slice, bool valid, int b) {
     const FEns& e = p.ens[ei];
     const int B = batch_of<BT>(p);
     const int lane = threadIdx.x & 31;
     float* A = p.arena;
     const int nw = (e.n + 31) >> 5;
-    const int cap = static_cast<int>(static_cast<size_t>(p.nmax) * DMAX * 4 / (32 * 2));  // uint16 per column
-    uint16_t* cntw = reinterpret_cast<uint16_t*>(ring);       // [word][column] spike counts (ring: free)
+    // the ring and queue regions (contiguous, free after the sweep): counts, lengths, lists
+    uint16_t* cntw = reinterpret_cast<uint16_t*>(ring);       // [word][column] spike counts
     int* stot = reinterpret_cast<int*>(ring) + nw * 16;       // [column] list lengths
-    uint16_t* list = reinterpret_cast<uint16_t*>(Ebuf);       // [position][column] (columns interleaved)
+    uint16_t* list = reinterpret_cast<uint16_t*>(stot + 32);  // [position][column] (columns interleaved)
+    const int cap = (lbytes - (nw * 64 + 128)) / 64;          // uint16 entries per column
     for (int w = slice; w < nw; w += kWarps) {
         const int i = w * 32 + lane;
         uint32_t bits = transpose32(i < e.n ? words[i] : 0u, lane);
@@ -1055,12 +1056,13 @@ __device__ void run_unit(const FusedProgram& p, int u, int k, bool do_update, bo
 
     // 3. decode: rows [r0, r0 + R) of this warp's tile over all neurons, ascending
     FTRACE(13, 0);
-    // One-tile units (B <= 32: the 8 warps are neuron slices of one tile) whose decoder
-    // products were staged separately: the slices compact each column's spiking neurons
-    // into an ascending index list (in the encoder region, free after the sweep), then
-    // every warp chains its own rows over the lists — all 8 warps decode instead of 2
-    const bool listed = active && p.tu == 1 && p.slices == kWarps && p.stage_dec &&
-                        decode_listed<DMAX, BT>(p, ei, k, last, S.ring, S.E, S.P, words, slice, valid, b);
+    // One-tile units (B <= 32: the 8 warps are neuron slices of one tile): the slices
+    // compact each column's spiking neurons into an ascending index list, then every
+    // thread chains (column, row) items over the lists — all 8 warps decode instead of 2
+    const bool listed = active && p.tu == 1 && p.slices == kWarps &&
+                        decode_listed<DMAX, BT>(p, ei, k, last, S.ring,
+                                                static_cast<int>(kWarps * kRingFloats * 4 + inq_bytes<DMAX>(p)),
+                                                p.stage_dec ? S.P : S.E, words, slice, valid, b);
     if (active && !listed) {
         const int dx = e.dx;
         int R = (dx + p.slices - 1) / p.slices;
