@@ -888,8 +888,8 @@ std::unique_ptr<FusedPlan> try_compile_fused(Engine& eng, std::string* why) {
         int64_t work = std::max<int64_t>(static_cast<int64_t>(ens_hi - ens_lo) * p.groups,
                                          (static_cast<int64_t>(p.n_conn) * B + 255) / 256);
         impl->grid = static_cast<int>(std::min<int64_t>(cap, std::max<int64_t>(1, work)));
-        if (const char* env = std::getenv("NENG_FUSED_GRID"))  // experiments: fewer co-resident CTAs
-            impl->grid = std::max(1, std::min(impl->grid, std::atoi(env)));
+        if (const char* env = std::getenv("NENG_FUSED_GRID"))  // experiments: co-resident CTAs (<= cap)
+            impl->grid = std::max(1, std::min(cap, std::atoi(env)));
 
         // barrier-free stepping (unsharded): claim order of the units
         impl->units = (ens_hi - ens_lo) * p.groups;
