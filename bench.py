@@ -211,11 +211,13 @@ def run_reference_arm(args):
         rp = refapi.planned_from_python(passes.run_passes(w.model))
         plan_note = f"repo planner (reference plan cache unavailable: {ex})"
     threads = os.cpu_count() or 1
-    steps = max(args.steps // 100, 2)  # bounded sample: a few timesteps of `threads` rows
-    warm = max(args.warmup // 5, 1)
+    # K timed steps after W warm-up steps, as the GPU arm; each step is a bounded sample of
+    # the workload: one timestep of `threads` batch rows (one single-row engine per host thread)
+    steps, warm = max(args.steps, 1), max(args.warmup, 1)
     secs = refapi.time_engines(rp, threads, 1, warm, steps, fp64=False, feed_seed=args.seed)
     value = threads * steps * neurons / secs
-    secs64 = refapi.time_engines(rp, threads, 1, warm, steps, fp64=True, feed_seed=args.seed)
+    steps64 = max(steps // 10, 2)  # EngineCore<double> (what run_bench times): a shorter sample
+    secs64 = refapi.time_engines(rp, threads, 1, warm, steps64, fp64=True, feed_seed=args.seed)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
             "warmup": warm, "ms_per_step": 1e3 * secs / steps * (args.batch / threads),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
@@ -225,7 +227,7 @@ def run_reference_arm(args):
                        "plan": plan_note, "feeds": "white noise N(0,1) on all 256 inputs", "cpu_model": cpu_model()},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                              "sample": f"{threads} rows x {steps} timesteps, one single-row engine per thread",
-                             "f64_value": threads * steps * neurons / secs64},
+                             "f64_value": threads * steps64 * neurons / secs64, "f64_steps": steps64},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
